@@ -1,0 +1,571 @@
+"""TEST INFRASTRUCTURE ONLY -- numpy restatement of the reference's sketched
+Hessenberg (sCMRH) / sketched LSLU (sLSLU) iteration loop.
+
+Every function cites the reference lines it restates (paths relative to the
+reference package ``pkg/src/hessketch``).  The restatement is parametrised by
+the working precision ``dtype``:
+
+* ``np.float64`` -- the reference itself.  With the same operator callables and
+  the same sketch matrices it reproduces the reference bit for bit (pinned by
+  ``tests/test_oracle_golden.py`` against fixtures generated from the reference).
+* ``np.float32`` -- "oracle32": identical algorithm, but the Krylov vectors
+  (r0, u, q, basis columns) and the elimination / pivot / normalisation
+  arithmetic are float32, as the device's fp32 path computes them.  Sketch
+  products, the projected least-squares solve and the iterate x = L_k y stay in
+  float64 (the device does the same).  The reference hard-casts to float64
+  (linops.py:109,115,119,125; hessenberg.py:164,282; solvers.py:418), so this
+  precision variant has no reference counterpart; it is pinned to the float64
+  path on problems where both must agree (see tests).
+
+Not a product path: nothing in ``paper_2502_02721_b200`` imports this module.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.linalg
+import scipy.sparse
+
+RANK_TOL = 1e-14  # linops.py:36
+
+
+class RankDeficiencyError(np.linalg.LinAlgError):
+    """linops.py:39-50."""
+
+    def __init__(self, message, rank):
+        super().__init__(message)
+        self.rank = rank
+
+
+class TrivialSolution(Exception):
+    """hessenberg.py:79-90."""
+
+    def __init__(self, message, x):
+        super().__init__(message)
+        self.x = x
+
+
+# ---------------------------------------------------------------------------
+# operators (linops.py:53-149)
+
+
+@dataclass
+class Counters:
+    """linops.py:53-68 (matvec, transpose, dot, sketch tallies)."""
+
+    matvecs: int = 0
+    tmatvecs: int = 0
+    dots: int = 0
+    sketches: int = 0
+
+    def snapshot(self):
+        return (self.matvecs, self.tmatvecs, self.dots, self.sketches)
+
+
+class Operator:
+    """Restates ``LinearOperator.apply``/``apply_transpose`` (linops.py:107-125):
+    length check, one count per application, result cast to the working dtype."""
+
+    def __init__(self, rows, cols, forward, transpose, dtype=np.float64):
+        self.rows, self.cols = int(rows), int(cols)
+        self.forward, self.transpose = forward, transpose
+        self.dtype = np.dtype(dtype)
+        self.counters = Counters()
+
+    @property
+    def is_square(self):
+        return self.rows == self.cols
+
+    def fresh(self):
+        return Operator(self.rows, self.cols, self.forward, self.transpose, self.dtype)
+
+    def apply(self, x):
+        x = np.asarray(x, dtype=self.dtype)
+        if x.shape != (self.cols,):
+            raise ValueError(f"operator expects a vector of length {self.cols}")
+        self.counters.matvecs += 1
+        return np.asarray(self.forward(x), dtype=self.dtype)
+
+    def apply_transpose(self, y):
+        y = np.asarray(y, dtype=self.dtype)
+        if y.shape != (self.rows,):
+            raise ValueError(f"operator transpose expects a vector of length {self.rows}")
+        self.counters.tmatvecs += 1
+        return np.asarray(self.transpose(y), dtype=self.dtype)
+
+
+def csr_operator(M, dtype=np.float64):
+    """``LinearOperator.from_matrix`` on a sparse matrix (linops.py:137-141):
+    forward ``M @ x`` and transpose ``M.T.tocsr() @ y``.  scipy's csr_matvec is
+    a sequential left-to-right row sum without FMA; with float32 data and a
+    float32 vector it runs in float32, with float64 it upcasts (exactly)."""
+    M = scipy.sparse.csr_matrix(M)
+    M.sort_indices()
+    Mt = M.T.tocsr()
+    if np.dtype(dtype) == np.float32:
+        M = M.astype(np.float32)
+        Mt = Mt.astype(np.float32)
+    return Operator(M.shape[0], M.shape[1], lambda x: M @ x, lambda y: Mt @ y, dtype)
+
+
+def dense_operator(M, dtype=np.float64, sequential=True):
+    """``LinearOperator.from_matrix`` on a dense array (linops.py:142-145).
+
+    The reference computes ``M @ x`` with BLAS dgemv, whose summation order is
+    library-defined.  ``sequential=True`` pins the order to a left-to-right row
+    sum without FMA (what the device dense kernel computes); ``False`` defers to
+    numpy's BLAS, i.e. the reference itself."""
+    M = np.asarray(M, dtype=dtype)
+    if M.ndim != 2:
+        raise ValueError("expected a 2-D matrix")
+    if not sequential:
+        return Operator(M.shape[0], M.shape[1], lambda x: M @ x, lambda y: M.T @ y, dtype)
+    Mt = np.ascontiguousarray(M.T)
+    return Operator(
+        M.shape[0], M.shape[1],
+        lambda x: sequential_rows(M, x), lambda y: sequential_rows(Mt, y), dtype,
+    )
+
+
+def sequential_rows(M, x):
+    """y_i = (((0 + M_i0 x_0) + M_i1 x_1) + ...) in M's dtype, no FMA."""
+    M = np.asarray(M)
+    x = np.asarray(x, dtype=M.dtype)
+    acc = np.zeros(M.shape[0], dtype=M.dtype)
+    for j in range(M.shape[1]):
+        acc = acc + M[:, j] * x[j]
+    return acc
+
+
+def identity_operator(n, dtype=np.float64):
+    """linops.py:147-149."""
+    return Operator(n, n, lambda x: x.copy(), lambda y: y.copy(), dtype)
+
+
+# ---------------------------------------------------------------------------
+# pivoting (hessenberg.py:93-129)
+
+
+def pivot_full(v, admissible):
+    """Full-scan ``pivot_select`` (hessenberg.py:93-115): argmax |v| over the
+    admissible set, ties to the smallest index, signed value; 0 => breakdown."""
+    admissible = np.asarray(admissible, dtype=np.int64)
+    if admissible.size == 0:
+        raise ValueError("admissible index set is empty")
+    mags = np.abs(v[admissible])
+    top = mags.max()
+    if top == 0.0:
+        return int(admissible.min()), 0.0
+    idx = int(admissible[mags == top].min())
+    return idx, v[idx]
+
+
+def _swap_to_position(perm, used, idx):
+    """hessenberg.py:127-129."""
+    pos = used + int(np.nonzero(perm[used:] == idx)[0][0])
+    perm[used], perm[pos] = perm[pos], perm[used]
+
+
+# ---------------------------------------------------------------------------
+# square process (hessenberg.py:132-226)
+
+
+@dataclass
+class SquareState:
+    L: list
+    h_cols: list
+    t: np.ndarray
+    beta: float
+    k: int
+    breakdown: bool
+    r0: np.ndarray
+    last_product: np.ndarray = None
+
+    def H_matrix(self, rows=None):
+        k = len(self.h_cols)
+        H = np.zeros((k + 1, k))
+        for j, col in enumerate(self.h_cols):
+            H[: j + 2, j] = col
+        return H if rows is None else H[:rows]
+
+
+def init_square(A, b, x0=None):
+    """hessenberg.py:160-188 (full pivoting)."""
+    if not A.is_square:
+        raise ValueError("the square Hessenberg process needs a square operator")
+    dt = A.dtype
+    b = np.asarray(b, dtype=dt)
+    if b.shape != (A.rows,):
+        raise ValueError(f"b must have length {A.rows}")
+    r0 = b.copy() if x0 is None else b - A.apply(np.asarray(x0, dtype=dt))
+    t = np.arange(A.rows)
+    idx, beta = pivot_full(r0, t)
+    if beta == 0.0:
+        x = np.zeros(A.cols) if x0 is None else np.asarray(x0, dtype=np.float64).copy()
+        raise TrivialSolution("initial residual is zero; starting point is exact", x)
+    _swap_to_position(t, 0, idx)
+    return SquareState([r0 / beta], [], t, beta, 0, False, r0)
+
+
+def _eliminate(u, basis, perm, k):
+    """The in-order elimination of hessenberg.py:209-212 / 347-350 / 371-374:
+    c_j = u[perm_j]; u <- u - c_j * basis_j (product rounded, then difference)."""
+    h = np.empty(k + 1)
+    for j in range(k):
+        c = u[perm[j]]
+        h[j] = c
+        u = u - c * basis[j]
+    return u, h
+
+
+def step_square(state, A, keep_product=True):
+    """hessenberg.py:191-226."""
+    if state.breakdown:
+        raise RuntimeError("factorization already broke down")
+    k = state.k + 1
+    n = A.rows
+    u = A.apply(state.L[-1])
+    if keep_product:
+        state.last_product = u.copy()
+    u, h = _eliminate(u, state.L, state.t, k)
+    if k < n:
+        idx, val = pivot_full(u, state.t[k:])
+    else:
+        val = 0.0
+    if val == 0.0:
+        h[k] = 0.0
+        state.breakdown = True
+    else:
+        h[k] = val
+        _swap_to_position(state.t, k, idx)
+        state.L.append(u / val)
+    state.h_cols.append(h)
+    state.k = k
+    return state
+
+
+# ---------------------------------------------------------------------------
+# generalized process (hessenberg.py:229-390)
+
+
+@dataclass
+class GenState:
+    D: list
+    L: list
+    h_cols: list
+    w_cols: list
+    t: np.ndarray
+    g: np.ndarray
+    beta: float
+    alpha: float
+    k: int
+    breakdown: bool
+    r0: np.ndarray
+    last_data_product: np.ndarray = None
+    last_solution_product: np.ndarray = None
+
+    def H_matrix(self, rows=None):
+        k = len(self.h_cols)
+        H = np.zeros((k + 1, k))
+        for j, col in enumerate(self.h_cols):
+            H[: j + 2, j] = col
+        return H if rows is None else H[:rows]
+
+    def W_matrix(self, rows=None):
+        cols = len(self.w_cols)
+        W = np.zeros((cols, cols))
+        for j, col in enumerate(self.w_cols):
+            W[: j + 1, j] = col
+        return W if rows is None else W[:rows]
+
+
+def init_generalized(A, b, x0=None):
+    """hessenberg.py:275-326 (full pivoting)."""
+    dt = A.dtype
+    b = np.asarray(b, dtype=dt)
+    if b.shape != (A.rows,):
+        raise ValueError(f"b must have length {A.rows}")
+    r0 = b.copy() if x0 is None else b - A.apply(np.asarray(x0, dtype=dt))
+    zero_x = np.zeros(A.cols) if x0 is None else np.asarray(x0, dtype=np.float64).copy()
+    t = np.arange(A.rows)
+    idx, beta = pivot_full(r0, t)
+    if beta == 0.0:
+        raise TrivialSolution("initial residual is zero; starting point is exact", zero_x)
+    d1 = r0 / beta
+    _swap_to_position(t, 0, idx)
+    v0 = A.apply_transpose(r0)
+    g = np.arange(A.cols)
+    idx2, alpha = pivot_full(v0, g)
+    if alpha == 0.0:
+        raise TrivialSolution(
+            "transposed residual is zero; the normal equations already hold", zero_x
+        )
+    l1 = v0 / alpha
+    _swap_to_position(g, 0, idx2)
+    r = A.apply_transpose(d1)
+    st = GenState([d1], [l1], [], [np.array([r[g[0]]], dtype=np.float64)], t, g,
+                  beta, alpha, 0, False, r0)
+    st.last_solution_product = r.copy()
+    return st
+
+
+def step_generalized(state, A, keep_products=True):
+    """hessenberg.py:329-390."""
+    if state.breakdown:
+        raise RuntimeError("factorization already broke down")
+    k = state.k + 1
+    m, n = A.rows, A.cols
+    u = A.apply(state.L[-1])
+    if keep_products:
+        state.last_data_product = u.copy()
+    u, h = _eliminate(u, state.D, state.t, k)
+    if k < m:
+        idx, val = pivot_full(u, state.t[k:])
+    else:
+        val = 0.0
+    if val == 0.0:
+        h[k] = 0.0
+        state.h_cols.append(h)
+        state.k = k
+        state.breakdown = True
+        return state
+    h[k] = val
+    _swap_to_position(state.t, k, idx)
+    d_new = u / val
+    state.D.append(d_new)
+    state.h_cols.append(h)
+
+    q = A.apply_transpose(d_new)
+    if keep_products:
+        state.last_solution_product = q.copy()
+    q, w = _eliminate(q, state.L, state.g, k)
+    if k < n:
+        idx2, val2 = pivot_full(q, state.g[k:])
+    else:
+        val2 = 0.0
+    if val2 == 0.0:
+        w[k] = 0.0
+        state.w_cols.append(w)
+        state.k = k
+        state.breakdown = True
+        return state
+    w[k] = val2
+    _swap_to_position(state.g, k, idx2)
+    state.L.append(q / val2)
+    state.w_cols.append(w)
+    state.k = k
+    return state
+
+
+# ---------------------------------------------------------------------------
+# sketches (sketch.py:43-65, 115-123)
+
+
+def gaussian_sketch_entries(out_rows, in_rows, seed):
+    """``make_gaussian_sketch`` (sketch.py:43-53): PCG64(seed) standard normals,
+    row-major (out_rows, in_rows), divided by sqrt(out_rows)."""
+    if out_rows < 1 or in_rows < 1:
+        raise ValueError("sketch dimensions must be positive")
+    gen = np.random.Generator(np.random.PCG64(seed))
+    return gen.standard_normal((out_rows, in_rows)) / np.sqrt(out_rows)
+
+
+def derive_seed(seed, stream):
+    """sketch.py:115-123."""
+    ss = np.random.SeedSequence(int(seed), spawn_key=(int(stream),))
+    return int(ss.generate_state(1, dtype=np.uint64)[0])
+
+
+def sketch_apply(S, v, counters):
+    """sketch.py:56-65: ``S @ v`` (float64) plus one sketch count."""
+    counters.sketches += 1
+    return np.asarray(S @ np.asarray(v, dtype=np.float64), dtype=np.float64)
+
+
+# ---------------------------------------------------------------------------
+# projected least squares (linops.py:168-229, solvers.py:204-225)
+
+
+def dense_qr_ls(M, rhs):
+    """linops.py:168-207: column-pivoted economic QR, rank gate, trsv."""
+    M = np.asarray(M, dtype=float)
+    rhs = np.asarray(rhs, dtype=float)
+    l, k = M.shape
+    if l < k:
+        raise ValueError("need at least as many rows as columns")
+    Q, R, piv = scipy.linalg.qr(M, mode="economic", pivoting=True)
+    diag = np.abs(np.diag(R))
+    largest = diag.max() if k else 0.0
+    if largest == 0.0 or diag.min() < RANK_TOL * largest:
+        rank = int(np.count_nonzero(diag >= RANK_TOL * largest)) if largest else 0
+        raise RankDeficiencyError("rank deficient", rank)
+    y_perm = scipy.linalg.solve_triangular(R, Q.T @ rhs)
+    y = np.empty(k)
+    y[piv] = y_perm
+    return y
+
+
+def stacked_tikhonov_ls(M, N, rhs, lam):
+    """linops.py:210-229: QR of [M; lam N] against [rhs; 0]; lam = 0 is dense_qr_ls."""
+    if lam == 0.0:
+        return dense_qr_ls(M, rhs)
+    stacked = np.vstack([M, lam * N])
+    srhs = np.concatenate([rhs, np.zeros(N.shape[0])])
+    return dense_qr_ls(stacked, srhs)
+
+
+def projected_solve(M, rhs, lam, N=None):
+    """solvers.py:204-218 (truncated lstsq fallback on rank deficiency)."""
+    try:
+        if lam == 0.0:
+            return dense_qr_ls(M, rhs), False
+        return stacked_tikhonov_ls(M, N, rhs, lam), False
+    except RankDeficiencyError:
+        if lam == 0.0:
+            stacked, srhs = M, rhs
+        else:
+            stacked = np.vstack([M, lam * N])
+            srhs = np.concatenate([rhs, np.zeros(N.shape[0])])
+        y, _, _, _ = np.linalg.lstsq(stacked, srhs, rcond=None)
+        return y, True
+
+
+def objective(M, rhs, y, lam, N=None):
+    """solvers.py:221-225."""
+    val = np.linalg.norm(M @ y - rhs) ** 2
+    if lam > 0.0:
+        val += lam**2 * np.linalg.norm(N @ y) ** 2
+    return float(np.sqrt(val))
+
+
+# ---------------------------------------------------------------------------
+# the loop driver (solvers.py:410-539, sketched branch)
+
+
+@dataclass
+class Result:
+    x: np.ndarray
+    records: list
+    termination: str
+    state: object = None
+    Z: np.ndarray = None
+    F: np.ndarray = None
+    sr0: np.ndarray = None
+    loop_seconds: float = 0.0
+
+    def column(self, name):
+        return [r[name] for r in self.records]
+
+
+def hessenberg_solve(
+    A, b, *, square, maxiter, ell=None, lam=0.0, seed=0, S2=None, S1=None,
+    x0=None, x_true=None, sketch_basis=False,
+):
+    """Restates ``_hessenberg_solve`` (solvers.py:410-539) for the sketched
+    solvers ``scmrh`` / ``slslu`` / ``*_tikhonov`` (solvers.py:562-605).
+
+    ``S2`` / ``S1``: explicit sketch matrices (anything supporting ``@``).  When
+    None they are drawn exactly as the reference draws them
+    (``make_gaussian_sketch(ell, A.rows, seed)`` and
+    ``make_gaussian_sketch(ell, A.cols, derive_seed(seed, 1))``, solvers.py:452-459).
+    Returns a :class:`Result` with per-iteration records carrying the
+    reference's TraceRecord fields.
+    """
+    if square and not A.is_square:
+        raise ValueError("this solver needs a square operator")
+    A = A.fresh()
+    c = A.counters
+    init = init_square if square else init_generalized
+    try:
+        state = init(A, b, x0=x0)
+    except TrivialSolution as sig:
+        return Result(x=sig.x, records=[], termination="trivial")
+
+    if S2 is not None:
+        if S2.shape[1] != A.rows:
+            raise ValueError("sketch/operator length mismatch")
+        ell = S2.shape[0]
+    elif ell is None:
+        ell = 10 * (maxiter + 1)  # solvers.py:113-116
+    if ell < maxiter + 1:  # solvers.py:447-451
+        raise ValueError(f"sketch_rows={ell} cannot embed a {maxiter}-dimensional projected problem")
+    if S2 is None:
+        S2 = gaussian_sketch_entries(ell, A.rows, seed)
+    keep = not sketch_basis
+    sr0 = sketch_apply(S2, state.r0, c)
+    Z_cols, G_cols, F_cols = [], [], []
+    if sketch_basis:
+        first = state.L[0] if square else state.D[0]
+        G_cols.append(sketch_apply(S2, first, c))
+    if lam > 0.0:
+        if S1 is None:
+            S1 = gaussian_sketch_entries(ell, A.cols, derive_seed(seed, 1))
+        F_cols.append(sketch_apply(S1, state.L[0], c))
+
+    records = []
+    termination = "maxiter"
+    x = None
+    x0_64 = None if x0 is None else np.asarray(x0, dtype=np.float64)
+    tic_all = time.perf_counter()
+    for k in range(1, maxiter + 1):
+        tic = time.perf_counter()
+        n_basis_before = len(state.L) if square else len(state.D)
+        n_sol_before = len(state.L)
+        if square:
+            step_square(state, A, keep_product=keep)
+            prod = state.last_product
+        else:
+            step_generalized(state, A, keep_products=keep)
+            prod = state.last_data_product
+        if keep:
+            Z_cols.append(sketch_apply(S2, prod, c))
+        else:
+            cols = state.L if square else state.D
+            if len(cols) > n_basis_before:
+                G_cols.append(sketch_apply(S2, cols[-1], c))
+        if lam > 0.0 and len(state.L) > n_sol_before:
+            F_cols.append(sketch_apply(S1, state.L[-1], c))
+
+        Lk = np.column_stack(state.L[:k]).astype(np.float64)
+        if sketch_basis:
+            G = np.column_stack(G_cols)
+            M = G @ state.H_matrix(rows=G.shape[1])
+        else:
+            M = np.column_stack(Z_cols)
+        N = np.column_stack(F_cols[:k]) if lam > 0.0 else None
+        y, fallback = projected_solve(M, sr0, lam, N)
+        x = Lk @ y
+        if x0_64 is not None:
+            x = x0_64 + x
+        rec = dict(
+            iteration=k,
+            proj_obj=objective(M, sr0, y, lam, N),
+            sres_norm=float(np.linalg.norm(M @ y - sr0)),
+            rel_err=None,
+            rank_fallback=fallback,
+        )
+        if x_true is not None:
+            xt = np.asarray(x_true, dtype=np.float64)
+            rec["rel_err"] = float(np.linalg.norm(x - xt) / np.linalg.norm(xt))
+        rec["matvecs"], rec["tmatvecs"], rec["dots"], rec["sketches"] = c.snapshot()
+        rec["wall_ms"] = (time.perf_counter() - tic) * 1e3
+        records.append(rec)
+        if state.breakdown:
+            termination = "breakdown"
+            break
+    loop_s = time.perf_counter() - tic_all
+    return Result(
+        x=x, records=records, termination=termination, state=state,
+        Z=np.column_stack(Z_cols) if Z_cols else None,
+        F=np.column_stack(F_cols) if F_cols else None, sr0=sr0, loop_seconds=loop_s,
+    )
+
+
+def pivots_of(state):
+    """Pivot sequences actually used: t[:len(basis)], g[:len(L)]."""
+    if isinstance(state, GenState):
+        return state.t[: len(state.D)].copy(), state.g[: len(state.L)].copy()
+    return state.t[: len(state.L)].copy(), None
