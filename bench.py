@@ -1,0 +1,307 @@
+#!/usr/bin/env python
+"""Benchmark: sketched-LSLU iterations/s at 2048^2 tomography (BASELINE.json
+config 4) and the achieved HBM bandwidth of the dominant kernel.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A "step" is one complete sLSLU solve of the config (K=300 iterations on the
+720 x 2897-ray, 2048^2-pixel exact-chord tomography operator, fp32 CSR with
+~3.8e9 nonzeros, sparse-sign S2 with ell=1200, zeta=8); the metric is
+iterations/s = 300 * steps / time.  ``value`` times the device loop with all
+inputs resident (CUDA events on the library's stream, max over ranks);
+``e2e`` times the public ``slslu(...)`` call with host b / x_true, including
+host<->device copies and the solver setup.  Inputs (A + A^T = 61 GB) are far
+larger than L2, so no flush is needed between steps.
+
+Multi-GPU: this version runs N independent replicas of the full problem
+(weak scaling, no data-path collective); the row-sharded NCCL path is
+described in DESIGN.md.
+
+``--impl reference`` times the CPU port of the reference loop
+(oracle/coracle.c, all host threads) on a bounded sample of the same
+workload (rank 0 only).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sketched-LSLU iterations/sec at 2048^2 tomography; achieved HBM GB/s"
+UNIT = "iterations/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    smax = float(parts[2])
+                except ValueError:
+                    continue
+                for name, flag in zip(names, parts[5:9]):
+                    if flag.lower() in ("active", "0x1", "1"):
+                        reasons.add(name)
+        except Exception:
+            pass
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def max_over_ranks(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([float(x)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def run_ours(args, ws, rank, local):
+    import numpy as np
+
+    import paper_2502_02721_b200 as hs
+    from paper_2502_02721_b200 import _lib
+    from paper_2502_02721_b200.problems import make_workload
+
+    os.environ["HS_DEVICE"] = str(local)
+    _lib.load()
+    ctx = _lib.context(local)
+    t_setup = time.perf_counter()
+    w = make_workload(args.config, seed=args.seed, scale=args.scale, maxiter=args.maxiter)
+    setup_s = time.perf_counter() - t_setup
+    K = w.cfg.maxiter
+    solve = hs.slslu if w.solver == "slslu" else hs.scmrh
+    op = w.operator
+    inf = op.info() if hasattr(op, "info") else {}
+
+    def one_step(x_true):
+        return solve(op, w.b, w.cfg, x_true=x_true, sketch=w.sketch)
+
+    for _ in range(args.warmup):
+        one_step(w.x_true)
+    ctx.synchronize()
+    barrier(ws)
+    ctx.reset_stats()
+    ctx.set_profiling(True)
+    launches0 = _lib.load().hs_launch_count()
+    loop_ms, wall_s, iters = [], [], 0
+    with ClockSampler(local) as clk:
+        barrier(ws)
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            res = one_step(w.x_true)  # host b / x_true in, host x / trace out
+            wall_s.append(time.perf_counter() - t0)
+            loop_ms.append(res.loop_ms)
+            iters += len(res.trace.records)
+        ctx.synchronize()
+        barrier(ws)
+    launches = _lib.load().hs_launch_count() - launches0
+    ctx.set_profiling(False)
+    stats = ctx.kernel_stats()
+    clocks = clk.summary()
+
+    tot_ms = max_over_ranks(sum(loop_ms), ws)
+    tot_wall = max_over_ranks(sum(wall_s), ws)
+    iters_all = iters * ws
+    value = iters_all / (tot_ms / 1e3)
+    e2e = iters_all / tot_wall
+    peak, peak_kind = _peaks()
+    # dominant kernel: the two order-faithful CSR SpMVs (A and A^T)
+    sp = [stats.get(k, {"launches": 0, "ms": 0.0, "bytes": 0.0}) for k in ("spmv_A", "spmv_AT")]
+    sp_launch = sum(s["launches"] for s in sp)
+    sp_ms = sum(s["ms"] for s in sp)
+    sp_bytes = sum(s["bytes"] for s in sp)
+    achieved = (sp_bytes / sp_launch) / ((sp_ms / sp_launch) / 1e3) / 1e9 if sp_launch else None
+    step_ms = tot_ms / args.steps
+    kernels = {k: {"launches": v["launches"], "ms_total": round(v["ms"], 3),
+                   "GBps": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1) if v["ms"] > 0 and v["bytes"] > 0 else None}
+               for k, v in stats.items()}
+    out = {
+        "metric": METRIC,
+        "value": round(value, 3),
+        "unit": UNIT,
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(step_ms, 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (seeded random-ellipse phantom, 1% noise; device-built exact-chord operator)",
+        "config": {
+            "workload": f"cfg{args.config}: " + w.name,
+            "grid": w.meta.get("grid"), "angles": w.meta.get("angles"), "bins": w.meta.get("bins"),
+            "nnz": inf.get("nnz"), "maxiter": K, "sketch": "sparse-sign ell=%d zeta=8" % w.cfg.sketch_rows,
+            "step": "one full sLSLU solve (maxiter iterations)",
+            "l2": "inputs (A + A^T) far larger than L2; no flush",
+            "parallelism": f"replicas{ws}" if ws > 1 else "single",
+        },
+        "e2e": {"value": round(e2e, 3), "unit": UNIT,
+                "h2d_bytes_per_step": int(w.b.nbytes + w.x_true.nbytes),
+                "d2h_bytes_per_step": int(w.x_true.nbytes + 8 * 12 * K)},
+        "roofline": {
+            "bound": "hbm",
+            "kernel": "csr_seq_spmv (A and A^T)",
+            "achieved": round(achieved, 1) if achieved else None,
+            "peak": peak,
+            "unit": "GB/s",
+            "frac": round(achieved / peak, 4) if achieved else None,
+            "peak_source": peak_kind,
+            "traffic": None,
+            "share_of_step": round(sp_ms / (sum(loop_ms)), 4) if loop_ms else None,
+        },
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "kernels": kernels,
+        "setup_s": round(setup_s, 2),
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args, w)
+    return out
+
+
+def cpu_baseline(args, w, seconds=None):
+    """Oracle port (oracle/coracle.c, OpenMP over host cores) on a bounded sample."""
+    try:
+        from oracle import cpu_baseline as cb
+
+        return cb.run(w, budget_s=seconds or args.cpu_seconds)
+    except Exception as e:  # reported, never fatal for the GPU number
+        return {"value": None, "unit": UNIT, "cores": None, "kind": "port", "sample": f"unavailable: {e}"}
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return None
+    from oracle import cpu_baseline as cb
+    from paper_2502_02721_b200.problems import make_workload
+
+    w = make_workload(args.config, seed=args.seed, scale=args.scale, maxiter=args.maxiter)
+    vals = []
+    last = None
+    for i in range(args.warmup + args.steps):
+        r = cb.run(w, budget_s=args.cpu_seconds)
+        if i >= args.warmup:
+            vals.append(r["value"])
+        last = r
+    value = statistics.mean(vals) if vals else None
+    return {
+        "metric": METRIC, "impl": "reference", "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": {"workload": f"cfg{args.config}", "sample": last["sample"] if last else None},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": last["cores"] if last else None, "kind": "port",
+                         "sample": last["sample"] if last else None},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--scale", type=int, default=None, help="image side override (testing)")
+    ap.add_argument("--maxiter", type=int, default=None)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+
+        backend = "gloo" if args.impl == "reference" else "nccl"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    if args.impl == "reference":
+        out = run_reference(args, ws, rank)
+    else:
+        out = run_ours(args, ws, rank, local)
+    if rank == 0 and out is not None:
+        print(json.dumps(out), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

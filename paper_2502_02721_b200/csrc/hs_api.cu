@@ -1,0 +1,907 @@
+// C-ABI of the B200 sketched-Hessenberg / sLSLU loop (include/hessketch_b200.h).
+//
+// The solve (hs_solve) restates _hessenberg_solve (solvers.py:410-539) for the
+// sketched solvers: a host loop issues, per iteration, the operator kernel,
+// the sketch kernel, the pivot-row forward substitution, ONE fused
+// elimination/argmax pass over the basis, the pivot commit and the
+// normalisation (twice for the rectangular process), then the cooperative
+// projected-solve kernel.  Nothing is copied back per iteration: breakdown and
+// all trace scalars live on the device and are read once at the end.
+#include <cuda_runtime.h>
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/hessketch_b200.h"
+#include "hs_build.cuh"
+#include "hs_common.cuh"
+#include "hs_loop.cuh"
+#include "hs_ops.cuh"
+#include "hs_qr.cuh"
+#include "hs_sketch.cuh"
+
+using namespace hs;
+
+// ---------------------------------------------------------------------------
+// errors
+
+static thread_local std::string g_err;
+
+namespace {
+
+struct HsError {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  throw HsError{code, buf};
+}
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) fail(HS_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call, \
+                                cudaGetErrorString(e_));                               \
+  } while (0)
+
+static unsigned long long g_launches = 0;  // kernels launched by this library (all streams)
+#define CKL()                   \
+  do {                          \
+    CK(cudaGetLastError());     \
+    ++g_launches;               \
+  } while (0)
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return HS_OK;
+  } catch (const HsError& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HS_ERR_RUNTIME;
+  }
+}
+
+size_t dsize(int dt) { return dt == HS_F64 ? 8 : (dt == HS_F32 ? 4 : 2); }
+long long round_up(long long a, long long b) { return (a + b - 1) / b * b; }
+
+// device buffer with RAII
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DBuf() = default;
+  explicit DBuf(size_t b, bool zero = true) { alloc(b, zero); }
+  void alloc(size_t b, bool zero = true) {
+    release();
+    bytes = b;
+    if (b) {
+      CK(cudaMalloc(&p, b));
+      if (zero) CK(cudaMemset(p, 0, b));
+    }
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  ~DBuf() { release(); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    release();
+    p = o.p; bytes = o.bytes; o.p = nullptr; o.bytes = 0;
+    return *this;
+  }
+  template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+int grid_for(long long work, int block, int cap) {
+  long long g = (work + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// context
+
+struct KStat {
+  long long launches = 0;
+  double ms = 0.0;
+  double bytes = 0.0;
+};
+
+struct hs_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  int nranks = 1, rank = 0;
+  bool profiling = false;
+  std::map<std::string, KStat> stats;
+  // pending event pairs for profiled launches
+  struct Pending {
+    std::string name;
+    cudaEvent_t a, b;
+    double bytes;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> free_events;
+
+  cudaEvent_t get_event() {
+    if (!free_events.empty()) {
+      cudaEvent_t e = free_events.back();
+      free_events.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    return e;
+  }
+  void harvest() {
+    if (pending.empty()) return;
+    CK(cudaStreamSynchronize(stream));
+    for (auto& p : pending) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, p.a, p.b));
+      auto& s = stats[p.name];
+      s.launches += 1;
+      s.ms += ms;
+      s.bytes += p.bytes;
+      free_events.push_back(p.a);
+      free_events.push_back(p.b);
+    }
+    pending.clear();
+  }
+};
+
+// scoped profiling bracket around one launch
+struct Prof {
+  hs_ctx* c;
+  const char* name;
+  double bytes;
+  cudaEvent_t a = nullptr;
+  Prof(hs_ctx* c_, const char* n, double b) : c(c_), name(n), bytes(b) {
+    if (c->profiling) {
+      a = c->get_event();
+      CK(cudaEventRecord(a, c->stream));
+    }
+  }
+  ~Prof() noexcept(false) {
+    if (c->profiling) {
+      cudaEvent_t b = c->get_event();
+      CK(cudaEventRecord(b, c->stream));
+      c->pending.push_back({name, a, b, bytes});
+      if (c->pending.size() > 4096) c->harvest();
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// operators
+
+enum { OP_DENSE = 0, OP_CSR = 1, OP_PSF = 2 };
+
+struct Csr {
+  long long rows = 0, cols = 0, nnz = 0;
+  DBuf rowptr, col, val;
+};
+
+struct hs_op {
+  hs_ctx* ctx = nullptr;
+  int kind = OP_DENSE;
+  int vdtype = HS_F64;
+  long long m = 0, n = 0;
+  // dense: column-major A (m x n) and column-major A^T (n x m)
+  DBuf Acm, Atcm;
+  // csr
+  Csr A, At;
+  // psf
+  int H = 0, W = 0, kh = 0, kw = 0;
+  DBuf K;
+
+  template <class V, class Tin, class T>
+  void apply_t(const void* x, void* y, bool transpose) const {
+    cudaStream_t s = ctx->stream;
+    const Tin* xi = reinterpret_cast<const Tin*>(x);
+    T* yo = reinterpret_cast<T*>(y);
+    if (kind == OP_CSR) {
+      const Csr& M = transpose ? At : A;
+      constexpr int WARPS = sizeof(T) == 8 ? 4 : 8, CH = 32;
+      const long long tiles = (M.rows + 31) / 32;
+      const int grid = grid_for(tiles, WARPS, ctx->num_sms * 64);
+      const double bytes = (double)M.nnz * (sizeof(V) + 4) + (double)(M.rows + 1) * 8 + (double)M.cols * sizeof(Tin) +
+                           (double)M.rows * sizeof(T);
+      Prof p(ctx, transpose ? "spmv_AT" : "spmv_A", bytes);
+      csr_seq_spmv_kernel<V, Tin, T, WARPS, CH><<<grid, WARPS * 32, 0, s>>>(
+          M.rows, M.rowptr.as<long long>(), M.col.as<int>(), M.val.as<V>(), xi, yo);
+      CKL();
+    } else if (kind == OP_DENSE) {
+      const long long rows = transpose ? n : m, cols = transpose ? m : n;
+      const V* Mcm = (transpose ? Atcm : Acm).as<V>();
+      Prof p(ctx, "dense_gemv", (double)rows * cols * sizeof(V));
+      dense_seq_gemv_kernel<V, Tin, T><<<grid_for(rows, 256, 1 << 30), 256, 1024 * sizeof(T), s>>>(rows, cols, Mcm,
+                                                                                                   xi, yo);
+      CKL();
+    } else {
+      constexpr int TX = 32, TY = 8;
+      dim3 grid((W + TX - 1) / TX, (H + TY - 1) / TY);
+      const size_t smem = ((size_t)(TX + 2 * (kw / 2)) * (TY + 2 * (kh / 2)) + (size_t)kh * kw) * sizeof(T);
+      Prof p(ctx, "psf_stencil", (double)H * W * (sizeof(Tin) + sizeof(T)));
+      if (smem > 48 * 1024)
+        CK(cudaFuncSetAttribute(psf_stencil_kernel<V, Tin, T, TX, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+      psf_stencil_kernel<V, Tin, T, TX, TY><<<grid, TX * TY, smem, s>>>(H, W, kh, kw, K.as<V>(), xi, yo,
+                                                                         transpose ? 1 : 0);
+      CKL();
+    }
+  }
+
+  // x: type xdt; y: type T (wdt)
+  void apply(const void* x, int xdt, void* y, int wdt, bool transpose) const {
+    if (wdt == HS_F64) {
+      if (xdt != HS_F64) fail(HS_ERR_TYPE, "fp64 work needs fp64 input vectors");
+      if (vdtype == HS_F64) apply_t<double, double, double>(x, y, transpose);
+      else apply_t<float, double, double>(x, y, transpose);
+    } else if (wdt == HS_F32) {
+      if (xdt == HS_F32) {
+        if (vdtype == HS_F64) apply_t<double, float, float>(x, y, transpose);
+        else apply_t<float, float, float>(x, y, transpose);
+      } else if (xdt == HS_BF16) {
+        if (vdtype == HS_F64) apply_t<double, __nv_bfloat16, float>(x, y, transpose);
+        else apply_t<float, __nv_bfloat16, float>(x, y, transpose);
+      } else {
+        fail(HS_ERR_TYPE, "fp32 work needs fp32/bf16 input vectors");
+      }
+    } else {
+      fail(HS_ERR_TYPE, "work dtype must be fp64 or fp32");
+    }
+  }
+
+  long long nnz_total() const { return kind == OP_CSR ? A.nnz : (kind == OP_DENSE ? m * n : 0); }
+};
+
+// build the transpose of a row-sorted CSR (rows x cols) on device: output rows
+// are the columns [cb, ce), each sorted by the original row index
+// (scipy M.T.tocsr() order).  `row_offset` is added to the stored keys.
+template <class V>
+static void csr_transpose(hs_ctx* ctx, const Csr& src, long long row_offset, long long cb, long long ce, Csr& dst) {
+  cudaStream_t s = ctx->stream;
+  const long long nr = ce - cb;
+  dst.rows = nr;
+  dst.cols = src.rows;  // caller fixes if row_offset != 0
+  DBuf cnt((nr + 1) * sizeof(unsigned int));
+  const int wpb = 8;
+  if (src.rows > 0) {
+    csr_colcount_kernel<<<grid_for(src.rows, wpb, 1 << 30), wpb * 32, 0, s>>>(
+        src.rows, src.rowptr.as<long long>(), src.col.as<int>(), cb, ce, cnt.as<unsigned int>());
+    CKL();
+  }
+  DBuf cnt64((nr + 1) * sizeof(long long));
+  u32_to_i64_kernel<<<grid_for(nr + 1, 256, 1 << 30), 256, 0, s>>>(nr + 1, cnt.as<unsigned int>(), cnt64.as<long long>());
+  CKL();
+  dst.rowptr.alloc((nr + 1) * sizeof(long long));
+  {
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt64.as<long long>(), dst.rowptr.as<long long>(), nr + 1, s));
+    DBuf t(tmp, false);
+    CK(cub::DeviceScan::ExclusiveSum(t.p, tmp, cnt64.as<long long>(), dst.rowptr.as<long long>(), nr + 1, s));
+  }
+  long long nnz = 0;
+  CK(cudaMemcpyAsync(&nnz, dst.rowptr.as<long long>() + nr, sizeof(long long), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  dst.nnz = nnz;
+  cnt.release();
+  cnt64.release();
+  DBuf cursor(nr * sizeof(unsigned long long), false);
+  i64_to_u64_kernel<<<grid_for(nr, 256, 1 << 30), 256, 0, s>>>(nr, dst.rowptr.as<long long>(),
+                                                               cursor.as<unsigned long long>());
+  CKL();
+  DBuf keys((size_t)std::max<long long>(nnz, 1) * sizeof(int), false);
+  DBuf vals((size_t)std::max<long long>(nnz, 1) * sizeof(V), false);
+  if (src.rows > 0) {
+    csr_scatter_kernel<V><<<grid_for(src.rows, wpb, 1 << 30), wpb * 32, 0, s>>>(
+        src.rows, row_offset, src.rowptr.as<long long>(), src.col.as<int>(), src.val.as<V>(), cb, ce,
+        cursor.as<unsigned long long>(), keys.as<int>(), vals.as<V>());
+    CKL();
+  }
+  cursor.release();
+  // sort each output row by key, in batches of rows with < 2^30 items
+  dst.col.alloc((size_t)std::max<long long>(nnz, 1) * sizeof(int), false);
+  dst.val.alloc((size_t)std::max<long long>(nnz, 1) * sizeof(V), false);
+  std::vector<long long> hptr(nr + 1);
+  CK(cudaMemcpyAsync(hptr.data(), dst.rowptr.p, (nr + 1) * sizeof(long long), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const long long kBatch = 1LL << 30;
+  long long r0 = 0;
+  while (r0 < nr) {
+    long long r1 = r0 + 1;
+    while (r1 < nr && hptr[r1 + 1] - hptr[r0] <= kBatch) ++r1;
+    const long long base = hptr[r0];
+    const long long items = hptr[r1] - base;
+    const int nseg = (int)(r1 - r0);
+    if (items > 0) {
+      // offsets relative to the batch base, as int
+      std::vector<int> off(nseg + 1);
+      for (int i = 0; i <= nseg; ++i) off[i] = (int)(hptr[r0 + i] - base);
+      DBuf doff((nseg + 1) * sizeof(int), false);
+      CK(cudaMemcpyAsync(doff.p, off.data(), (nseg + 1) * sizeof(int), cudaMemcpyHostToDevice, s));
+      size_t tmp = 0;
+      CK(cub::DeviceSegmentedSort::SortPairs(nullptr, tmp, keys.as<int>() + base, dst.col.as<int>() + base,
+                                             vals.as<V>() + base, dst.val.as<V>() + base, (int)items, nseg,
+                                             doff.as<int>(), doff.as<int>() + 1, s));
+      DBuf t(tmp, false);
+      CK(cub::DeviceSegmentedSort::SortPairs(t.p, tmp, keys.as<int>() + base, dst.col.as<int>() + base,
+                                             vals.as<V>() + base, dst.val.as<V>() + base, (int)items, nseg,
+                                             doff.as<int>(), doff.as<int>() + 1, s));
+      CK(cudaStreamSynchronize(s));
+    }
+    r0 = r1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// sketches
+
+struct hs_sketch {
+  hs_ctx* ctx = nullptr;
+  int kind = HS_SKETCH_DENSE;
+  long long ell = 0, m = 0;
+  unsigned long long seed = 0;
+  int zeta = 0;
+  DBuf S;                 // dense row-major fp64
+  DBuf rowptr, scol;      // sparse sign, by sketch row (also CSR kind: cols)
+  DBuf cval;              // CSR kind: fp64 values
+  DBuf part;              // gaussian tile partials
+  long long tile_cols = 0;
+  int ntiles = 0;
+  uint2 key() const { return make_uint2((unsigned)seed, (unsigned)(seed >> 32)); }
+
+  template <class Tin>
+  void apply_t(const void* v, double* z) const {
+    cudaStream_t s = ctx->stream;
+    const Tin* vi = reinterpret_cast<const Tin*>(v);
+    if (kind == HS_SKETCH_DENSE) {
+      Prof p(ctx, "sketch_dense", (double)ell * m * 8);
+      sketch_dense_kernel<double, Tin><<<(int)ell, 256, 0, s>>>((int)ell, m, S.as<double>(), m, vi, z);
+      CKL();
+    } else if (kind == HS_SKETCH_GAUSSIAN) {
+      Prof p(ctx, "sketch_gauss", (double)m * sizeof(Tin));
+      const int nq = (int)((ell + 3) / 4);
+      dim3 grid(ntiles, (nq + 63) / 64);
+      sketch_gauss_partial_kernel<Tin><<<grid, 256, 0, s>>>((int)ell, m, 0, tile_cols, key(), vi, part.as<double>());
+      CKL();
+      sketch_tile_reduce_kernel<<<grid_for(ell, 128, 1 << 30), 128, 0, s>>>((int)ell, ntiles, part.as<double>(),
+                                                                            1.0 / std::sqrt((double)ell), z);
+      CKL();
+    } else if (kind == 3) {
+      Prof p(ctx, "sketch_csr", 0.0);
+      sketch_csr_kernel<Tin><<<(int)ell, 256, 0, s>>>((int)ell, rowptr.as<long long>(), scol.as<int>(),
+                                                      cval.as<double>(), vi, z);
+      CKL();
+    } else {
+      Prof p(ctx, "sketch_sparse", (double)m * zeta * 4 + (double)m * sizeof(Tin));
+      sketch_sparse_kernel<Tin><<<(int)ell, 256, 0, s>>>((int)ell, rowptr.as<long long>(), scol.as<int>(), 0, m, vi,
+                                                         1.0 / std::sqrt((double)zeta), z);
+      CKL();
+    }
+  }
+  void apply(const void* v, int vdt, double* z) const {
+    if (vdt == HS_F64) apply_t<double>(v, z);
+    else if (vdt == HS_F32) apply_t<float>(v, z);
+    else apply_t<__nv_bfloat16>(v, z);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// result
+
+struct hs_result {
+  int n_records = 0, termination = HS_TERM_MAXITER, k = 0, bd_side = -1;
+  int n_basis_data = 0, n_basis_sol = 0;
+  bool square = true;
+  long long m = 0, n = 0, ell = 0;
+  int basis_dtype = HS_F64;
+  std::vector<double> x, sres, proj, relerr, wall_ms, H, W, Z, sr0, y;
+  std::vector<int> rankfb;
+  std::vector<long long> matvecs, tmatvecs, dots, sketches, t, g;
+  double loop_ms = 0.0;
+  // device-resident bases kept for on-demand export
+  std::shared_ptr<DBuf> Lb, Db;
+  long long ldn = 0, ldm = 0;
+  hs_ctx* ctx = nullptr;
+};
+
+// ---------------------------------------------------------------------------
+// the solver
+
+namespace {
+
+template <class T, class B>
+struct Solver {
+  static constexpr int VEC = 16 / sizeof(B);
+  hs_ctx* ctx;
+  hs_op* op;
+  const hs_config cfg;
+  hs_sketch* S2;
+  hs_sketch* S1;
+  int wdt, bdt;
+
+  Solver(hs_ctx* c, hs_op* o, const hs_config& cf, hs_sketch* s2, hs_sketch* s1, int w, int b)
+      : ctx(c), op(o), cfg(cf), S2(s2), S1(s1), wdt(w), bdt(b) {}
+
+  void fsub(const T* u, const long long* pos, const T* P, int ldp, int k, int iter, int side, T* c,
+            double* hcol) {
+    if (k == 0) return;
+    cudaStream_t s = ctx->stream;
+    if (k <= 8 * 32) fsub_warp_kernel<T, 8><<<1, 32, 0, s>>>(u, pos, 0, P, ldp, nullptr, k, st, iter, side, c, hcol);
+    else if (k <= 32 * 32)
+      fsub_warp_kernel<T, 32><<<1, 32, 0, s>>>(u, pos, 0, P, ldp, nullptr, k, st, iter, side, c, hcol);
+    else fail(HS_ERR_NOTIMPL, "maxiter above 1023 is not supported");
+    CKL();
+  }
+
+  LoopState* st = nullptr;
+
+  void run(const double* b_h, const double* x0_h, const double* xt_h, hs_result* res) {
+    cudaStream_t s = ctx->stream;
+    const bool square = cfg.square != 0;
+    const int K = cfg.maxiter;
+    const long long m = op->m, n = op->n;
+    const long long ell = S2->ell;
+    const bool lamon = cfg.lam > 0.0;
+    const bool sb = cfg.sketch_basis != 0;
+    const long long ldm = round_up(m, 64), ldn = round_up(n, 64);
+    const int ldp = K + 2;
+    const int Ls = (int)(lamon ? 2 * ell : ell);
+    const int ldq = (int)round_up(Ls, 32);
+    const int SMS = ctx->num_sms;
+    const int ELIM_CAP = SMS * 8;
+
+    // ---- buffers
+    auto Lb = std::make_shared<DBuf>((size_t)(K + 1) * ldn * sizeof(B));
+    std::shared_ptr<DBuf> Db;
+    if (!square) Db = std::make_shared<DBuf>((size_t)(K + 2) * ldm * sizeof(B));
+    DBuf u(ldm * sizeof(T)), q(ldn * sizeof(T)), r0(ldm * sizeof(T)), bT(ldm * sizeof(T));
+    DBuf bd(m * sizeof(double), false), x0d, xtd, xd(n * sizeof(double));
+    DBuf Hb((size_t)(K + 1) * K * sizeof(double)), Wb((size_t)(K + 2) * (K + 1) * sizeof(double));
+    DBuf PD((size_t)ldp * ldp * sizeof(T)), PL((size_t)ldp * ldp * sizeof(T));
+    DBuf tpos(ldp * sizeof(long long)), gpos(ldp * sizeof(long long));
+    DBuf cvec(ldp * sizeof(T)), pv(2 * sizeof(T));
+    DBuf Zb((size_t)ell * K * sizeof(double)), Fb((size_t)ell * (K + 1) * sizeof(double)),
+        Gb((size_t)ell * (K + 2) * sizeof(double)), sr0(ell * sizeof(double));
+    DBuf Qb((size_t)ldq * K * sizeof(double)), Rinv((size_t)K * K * sizeof(double)), Rdiag(K * sizeof(double)),
+        yb(K * sizeof(double)), Yh((size_t)K * K * sizeof(double));
+    const int NB = std::max(1, std::min(64, (Ls + 47) / 48));
+    DBuf part((size_t)4 * NB * (K + 2) * sizeof(double));
+    DBuf sresb(K * sizeof(double)), projb(K * sizeof(double)), rfb(K * sizeof(int)), rel2((K + 1) * sizeof(double));
+    DBuf candp((size_t)std::max(ELIM_CAP, 4096) * sizeof(Cand)), xpart((size_t)std::max(ELIM_CAP, 4096) * sizeof(double));
+    DBuf stb(sizeof(LoopState));
+    st = stb.as<LoopState>();
+    LoopState hst;
+
+    CK(cudaMemcpyAsync(bd.p, b_h, m * sizeof(double), cudaMemcpyHostToDevice, s));
+    if (x0_h) {
+      x0d.alloc(n * sizeof(double), false);
+      CK(cudaMemcpyAsync(x0d.p, x0_h, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    }
+    double xt_norm = 0.0;
+    if (xt_h) {
+      xtd.alloc(n * sizeof(double), false);
+      CK(cudaMemcpyAsync(xtd.p, xt_h, n * sizeof(double), cudaMemcpyHostToDevice, s));
+      double acc = 0.0;
+      for (long long i = 0; i < n; ++i) acc += xt_h[i] * xt_h[i];
+      xt_norm = std::sqrt(acc);
+      if (xt_norm == 0.0) fail(HS_ERR_VALUE, "x_true must be nonzero for relative errors");
+    }
+    convert_kernel<T, double><<<grid_for(m, 256, SMS * 16), 256, 0, s>>>(m, bd.as<double>(), bT.as<T>());
+    CKL();
+
+    B* L = Lb->template as<B>();
+    B* D = square ? nullptr : Db->template as<B>();
+    auto Lcol = [&](int j) { return L + (long long)j * ldn; };
+    auto Dcol = [&](int j) { return D + (long long)j * ldm; };
+    double* H = Hb.as<double>();
+    double* Wm = Wb.as<double>();
+    auto Hcol = [&](int j) { return H + (long long)j * (K + 1); };
+    auto Wcol = [&](int j) { return Wm + (long long)j * (K + 2); };
+
+    // ---- r0 = b (or b - A x0), hessenberg.py:163-168 / 281-288
+    int matvec0 = 0;
+    if (x0_h) {
+      DBuf x0T(ldn * sizeof(T));
+      convert_kernel<T, double><<<grid_for(n, 256, SMS * 16), 256, 0, s>>>(n, x0d.as<double>(), x0T.as<T>());
+      CKL();
+      op->apply(x0T.p, wdt, r0.p, wdt, false);
+      sub_kernel<T><<<grid_for(m, 256, SMS * 16), 256, 0, s>>>(m, bT.as<T>(), r0.as<T>());
+      CKL();
+      CK(cudaStreamSynchronize(s));
+      matvec0 = 1;
+    } else {
+      CK(cudaMemcpyAsync(r0.p, bT.p, m * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    }
+
+    auto trivial = [&]() {
+      res->termination = HS_TERM_TRIVIAL;
+      res->n_records = 0;
+      res->x.assign(n, 0.0);
+      if (x0_h) std::copy(x0_h, x0_h + n, res->x.begin());
+    };
+    auto argmax_host = [&](const T* v, long long len, int side, double& val, long long& idx) {
+      const int g = grid_for(len, 256, SMS * 4);
+      argmax_kernel<T><<<g, 256, 0, s>>>(len, 0, v, candp.as<Cand>(), st, side);
+      CKL();
+      CK(cudaMemcpyAsync(&hst, st, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      val = hst.piv_val[side];
+      idx = hst.piv_idx[side];
+    };
+    auto set_pivot = [&](T* pvslot, double val) {
+      T tv = (T)val;
+      CK(cudaMemcpyAsync(pvslot, &tv, sizeof(T), cudaMemcpyHostToDevice, s));
+    };
+    auto set_pos_and_unit = [&](long long* pos, T* P, long long idx) {
+      T one = T(1);
+      CK(cudaMemcpyAsync(pos, &idx, sizeof(long long), cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(P, &one, sizeof(T), cudaMemcpyHostToDevice, s));
+      CK(cudaStreamSynchronize(s));
+    };
+    const int NORM_G = SMS * 8;
+
+    int tmat0 = 0, sk0 = 0;
+    double beta, alpha = 0.0;
+    long long idx;
+    argmax_host(r0.as<T>(), m, 0, beta, idx);
+    if (beta == 0.0) {
+      trivial();
+      return;
+    }
+    B* first_basis;  // d1 (rect) or l1 (square)
+    if (square) {
+      set_pos_and_unit(tpos.as<long long>(), PL.as<T>(), idx);
+      set_pivot(pv.as<T>(), beta);
+      normalize_kernel<T, B><<<grid_for(ldn, 256, NORM_G), 256, 0, s>>>(n, ldn, r0.as<T>(), pv.as<T>(), Lcol(0), st, 0, 0);
+      CKL();
+      first_basis = Lcol(0);
+    } else {
+      set_pos_and_unit(tpos.as<long long>(), PD.as<T>(), idx);
+      set_pivot(pv.as<T>(), beta);
+      normalize_kernel<T, B><<<grid_for(ldm, 256, NORM_G), 256, 0, s>>>(m, ldm, r0.as<T>(), pv.as<T>(), Dcol(0), st, 0, 0);
+      CKL();
+      first_basis = Dcol(0);
+      // v0 = A^T r0
+      op->apply(r0.p, wdt, q.p, wdt, true);
+      tmat0++;
+      long long idx2;
+      argmax_host(q.as<T>(), n, 1, alpha, idx2);
+      if (alpha == 0.0) {
+        trivial();
+        return;
+      }
+      set_pos_and_unit(gpos.as<long long>(), PL.as<T>(), idx2);
+      set_pivot(pv.as<T>() + 1, alpha);
+      normalize_kernel<T, B><<<grid_for(ldn, 256, NORM_G), 256, 0, s>>>(n, ldn, q.as<T>(), pv.as<T>() + 1, Lcol(0), st, 1, 0);
+      CKL();
+      // r = A^T d1, W(1,1) = r[g0]
+      op->apply(Dcol(0), bdt, q.p, wdt, true);
+      tmat0++;
+      T w00;
+      CK(cudaMemcpyAsync(&w00, q.as<T>() + idx2, sizeof(T), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      double w00d = (double)w00;
+      CK(cudaMemcpyAsync(Wcol(0), &w00d, sizeof(double), cudaMemcpyHostToDevice, s));
+    }
+    // sketch setup (solvers.py:454-463)
+    S2->apply(r0.p, wdt, sr0.as<double>());
+    sk0++;
+    if (sb) {
+      S2->apply(first_basis, bdt, Gb.as<double>());
+      sk0++;
+    }
+    if (lamon) {
+      S1->apply(Lcol(0), bdt, Fb.as<double>());
+      sk0++;
+    }
+
+    // ---- the loop (solvers.py:468-538)
+    std::vector<cudaEvent_t> ev(K + 1);
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    QrArgs qa;
+    qa.ell = (int)ell; qa.Ls = Ls; qa.ldq = ldq; qa.kmax = K; qa.lam = cfg.lam;
+    qa.Z = Zb.as<double>(); qa.F = lamon ? Fb.as<double>() : nullptr; qa.sr0 = sr0.as<double>();
+    qa.Q = Qb.as<double>(); qa.Rinv = Rinv.as<double>(); qa.Rdiag = Rdiag.as<double>(); qa.y = yb.as<double>();
+    qa.Yhist = Yh.as<double>(); qa.part = part.as<double>(); qa.sres = sresb.as<double>(); qa.proj = projb.as<double>();
+    qa.rankfb = rfb.as<int>(); qa.st = st;
+    const size_t qr_smem = ((size_t)((Ls + NB - 1) / NB) + 2 * (size_t)K) * sizeof(double);
+    if (qr_smem > 48 * 1024)
+      CK(cudaFuncSetAttribute(qr_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qr_smem));
+    const bool rec_x = cfg.record_x && xt_h;
+    const size_t elim_smem_base = 16;
+    auto elim = [&](T* vec, long long len, long long ldv, const B* basis, int k, int side, int iter, int kx,
+                    const double* yx, double* relerr_slot) {
+      const long long nvec = (len + VEC - 1) / VEC;
+      const int g = grid_for(nvec, 256, ELIM_CAP);
+      const size_t smem = ((k * sizeof(T) + 15) / 16) * 16 + (size_t)kx * sizeof(double) + elim_smem_base;
+      const double bytes = (double)std::max(k, kx) * len * sizeof(B) + 2.0 * len * sizeof(T) +
+                           (kx ? (double)len * 8 : 0.0);
+      Prof p(ctx, side == 0 && !square ? "elim_D" : "elim_L", bytes);
+      if (smem > 48 * 1024)
+        CK(cudaFuncSetAttribute(elim_pass_kernel<T, B, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      (void)ldv;
+      elim_pass_kernel<T, B, VEC><<<g, 256, smem, s>>>(
+          len, 0, basis, square || side == 1 ? ldn : ldm, nullptr, k, cvec.as<T>(), vec, kx, yx, nullptr,
+          x0_h ? x0d.as<double>() : nullptr, kx ? xtd.as<double>() : nullptr, xpart.as<double>(), relerr_slot,
+          candp.as<Cand>(), st, side, iter, 1);
+      CKL();
+    };
+
+    // host-side breakdown polling (pinned flag copied at the end of each iteration)
+    int* hflag = nullptr;
+    CK(cudaMallocHost(&hflag, sizeof(int) * (K + 1)));
+    for (int i = 0; i <= K; ++i) hflag[i] = 0;
+    std::vector<cudaEvent_t> flag_ev(K + 1);
+    for (auto& e : flag_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+
+    CK(cudaEventRecord(ev[0], s));
+    int k_last = 0;
+    int bd_at = 0;
+    for (int k = 1; k <= K; ++k) {
+      // stop launching once a breakdown two iterations back is visible
+      if (k >= 3) {
+        CK(cudaEventSynchronize(flag_ev[k - 2]));
+        if (hflag[k - 2] != 0) break;
+      }
+      k_last = k;
+      const int kx = (rec_x && k >= 2) ? k - 1 : 0;
+      const double* yprev = kx ? Yh.as<double>() + (long long)(k - 2) * K : nullptr;
+      double* relslot = kx ? rel2.as<double>() + (k - 2) : nullptr;
+      if (!square) {
+        op->apply(Lcol(k - 1), bdt, u.p, wdt, false);
+        if (!sb) S2->apply(u.p, wdt, Zb.as<double>() + (long long)(k - 1) * ell);
+        fsub(u.as<T>(), tpos.as<long long>(), PD.as<T>(), ldp, k, k, 0, cvec.as<T>(), Hcol(k - 1));
+        elim(u.as<T>(), m, ldm, D, k, 0, k, 0, nullptr, nullptr);
+        pivot_commit_kernel<T, B><<<1, 256, 0, s>>>(k, m, Hcol(k - 1), tpos.as<long long>(), PD.as<T>(), ldp, D, ldm,
+                                                    0, m, st, 0, k, pv.as<T>());
+        CKL();
+        normalize_kernel<T, B><<<grid_for(ldm, 256, NORM_G), 256, 0, s>>>(m, ldm, u.as<T>(), pv.as<T>(), Dcol(k), st, 0, k);
+        CKL();
+        if (sb) S2->apply(Dcol(k), bdt, Gb.as<double>() + (long long)k * ell);
+        op->apply(Dcol(k), bdt, q.p, wdt, true);
+        fsub(q.as<T>(), gpos.as<long long>(), PL.as<T>(), ldp, k, k, 1, cvec.as<T>(), Wcol(k));
+        elim(q.as<T>(), n, ldn, L, k, 1, k, kx, yprev, relslot);
+        pivot_commit_kernel<T, B><<<1, 256, 0, s>>>(k, n, Wcol(k), gpos.as<long long>(), PL.as<T>(), ldp, L, ldn, 0,
+                                                    n, st, 1, k, pv.as<T>() + 1);
+        CKL();
+        normalize_kernel<T, B><<<grid_for(ldn, 256, NORM_G), 256, 0, s>>>(n, ldn, q.as<T>(), pv.as<T>() + 1, Lcol(k), st, 1, k);
+        CKL();
+      } else {
+        op->apply(Lcol(k - 1), bdt, u.p, wdt, false);
+        if (!sb) S2->apply(u.p, wdt, Zb.as<double>() + (long long)(k - 1) * ell);
+        fsub(u.as<T>(), tpos.as<long long>(), PL.as<T>(), ldp, k, k, 0, cvec.as<T>(), Hcol(k - 1));
+        elim(u.as<T>(), n, ldn, L, k, 0, k, kx, yprev, relslot);
+        pivot_commit_kernel<T, B><<<1, 256, 0, s>>>(k, n, Hcol(k - 1), tpos.as<long long>(), PL.as<T>(), ldp, L, ldn,
+                                                    0, n, st, 0, k, pv.as<T>());
+        CKL();
+        normalize_kernel<T, B><<<grid_for(ldn, 256, NORM_G), 256, 0, s>>>(n, ldn, u.as<T>(), pv.as<T>(), Lcol(k), st, 0, k);
+        CKL();
+        if (sb) S2->apply(Lcol(k), bdt, Gb.as<double>() + (long long)k * ell);
+      }
+      if (lamon) S1->apply(Lcol(k), bdt, Fb.as<double>() + (long long)k * ell);
+      if (sb) {
+        // M column k-1 = G[:, :k+1] @ H[:k+1, k-1]  (zero columns/entries past a breakdown)
+        gemv_small_kernel<<<grid_for(ell, 128, 1 << 30), 128, 0, s>>>((int)ell, k + 1, Gb.as<double>(), Hcol(k - 1),
+                                                                       Zb.as<double>() + (long long)(k - 1) * ell);
+        CKL();
+      }
+      qa.zcol = Zb.as<double>() + (long long)(k - 1) * ell;
+      qa.fcol = lamon ? Fb.as<double>() + (long long)(k - 1) * ell : nullptr;
+      {
+        Prof p(ctx, "qr_step", 0.0);
+        int kk = k, it = k;
+        void* args[] = {&qa, &kk, &it};
+        CK(cudaLaunchCooperativeKernel((void*)qr_step_kernel, dim3(NB), dim3(256), args, qr_smem, s));
+        ++g_launches;
+      }
+      CK(cudaEventRecord(ev[k], s));
+      CK(cudaMemcpyAsync(hflag + k, &st->bd_iter, sizeof(int), cudaMemcpyDeviceToHost, s));
+      CK(cudaEventRecord(flag_ev[k], s));
+    }
+    CK(cudaStreamSynchronize(s));
+    CK(cudaMemcpy(&hst, st, sizeof(LoopState), cudaMemcpyDeviceToHost));
+    bd_at = hst.bd_iter;
+    const int kend = bd_at ? bd_at : k_last;
+    res->k = kend;
+    res->n_records = kend;
+    res->termination = bd_at ? HS_TERM_BREAKDOWN : HS_TERM_MAXITER;
+    res->bd_side = bd_at ? hst.bd_side : -1;
+
+    // ---- final iterate(s): x_kend, and x_{kend-1} when the fused pass skipped it
+    auto xpass = [&](int kx, double* xout, double* relslot) {
+      const int g = grid_for(n, 256, SMS * 8);
+      Prof p(ctx, "xpass", (double)kx * n * sizeof(B) + 16.0 * n);
+      xpass_kernel<B><<<g, 256, (size_t)kx * sizeof(double), s>>>(n, L, ldn, kx, Yh.as<double>() + (long long)(kx - 1) * K,
+                                                                  x0_h ? x0d.as<double>() : nullptr,
+                                                                  xt_h ? xtd.as<double>() : nullptr, xout,
+                                                                  xpart.as<double>(), relslot, st);
+      CKL();
+    };
+    xpass(kend, xd.as<double>(), xt_h ? rel2.as<double>() + (kend - 1) : nullptr);
+    const bool data_bd = bd_at && !square && hst.bd_side == 0;
+    if (rec_x && kend >= 2 && data_bd) xpass(kend - 1, nullptr, rel2.as<double>() + (kend - 2));
+    CK(cudaStreamSynchronize(s));
+    float lms = 0;
+    CK(cudaEventElapsedTime(&lms, ev[0], ev[kend]));
+    res->loop_ms = lms;
+    res->wall_ms.resize(kend);
+    for (int k = 1; k <= kend; ++k) {
+      float w = 0;
+      CK(cudaEventElapsedTime(&w, ev[k - 1], ev[k]));
+      res->wall_ms[k - 1] = w;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    for (auto& e : flag_ev) cudaEventDestroy(e);
+    cudaFreeHost(hflag);
+
+    // ---- copy back
+    res->x.resize(n);
+    CK(cudaMemcpy(res->x.data(), xd.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+    res->sres.resize(kend);
+    res->proj.resize(kend);
+    res->rankfb.resize(kend);
+    CK(cudaMemcpy(res->sres.data(), sresb.p, kend * sizeof(double), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(res->proj.data(), projb.p, kend * sizeof(double), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(res->rankfb.data(), rfb.p, kend * sizeof(int), cudaMemcpyDeviceToHost));
+    res->relerr.assign(kend, NAN);
+    if (xt_h) {
+      std::vector<double> r2(K + 1);
+      CK(cudaMemcpy(r2.data(), rel2.p, (K + 1) * sizeof(double), cudaMemcpyDeviceToHost));
+      for (int k = 1; k <= kend; ++k)
+        if (rec_x || k == kend) res->relerr[k - 1] = std::sqrt(r2[k - 1]) / xt_norm;
+    }
+    // H (k+1) x k, W
+    res->H.assign((size_t)(kend + 1) * kend, 0.0);
+    {
+      std::vector<double> hb((size_t)(K + 1) * K);
+      CK(cudaMemcpy(hb.data(), Hb.p, hb.size() * sizeof(double), cudaMemcpyDeviceToHost));
+      for (int j = 0; j < kend; ++j)
+        for (int i = 0; i <= j + 1 && i <= kend; ++i) res->H[(size_t)j * (kend + 1) + i] = hb[(size_t)j * (K + 1) + i];
+    }
+    // basis sizes (hessenberg.py: D grows unless the data side broke down, L unless any side did)
+    const int grew_last_D = (bd_at && (square || hst.bd_side == 0)) ? 0 : 1;
+    const int grew_last_L = bd_at ? 0 : 1;
+    if (square) {
+      res->n_basis_sol = 1 + (kend - 1) + grew_last_L;
+      res->n_basis_data = res->n_basis_sol;
+    } else {
+      res->n_basis_data = 1 + (kend - 1) + grew_last_D;
+      res->n_basis_sol = 1 + (kend - 1) + grew_last_L;
+      const int nw = res->n_basis_data;  // W has one column per D column
+      res->W.assign((size_t)nw * nw, 0.0);
+      std::vector<double> wb((size_t)(K + 2) * (K + 1));
+      CK(cudaMemcpy(wb.data(), Wb.p, wb.size() * sizeof(double), cudaMemcpyDeviceToHost));
+      for (int j = 0; j < nw; ++j)
+        for (int i = 0; i <= j; ++i) res->W[(size_t)j * nw + i] = wb[(size_t)j * (K + 2) + i];
+    }
+    {
+      std::vector<long long> tp(ldp), gp(ldp);
+      CK(cudaMemcpy(tp.data(), tpos.p, ldp * sizeof(long long), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(gp.data(), gpos.p, ldp * sizeof(long long), cudaMemcpyDeviceToHost));
+      if (square) {
+        res->t.assign(tp.begin(), tp.begin() + res->n_basis_sol);
+      } else {
+        res->t.assign(tp.begin(), tp.begin() + res->n_basis_data);
+        res->g.assign(gp.begin(), gp.begin() + res->n_basis_sol);
+      }
+    }
+    res->Z.resize((size_t)ell * kend);
+    CK(cudaMemcpy(res->Z.data(), Zb.p, res->Z.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    res->sr0.resize(ell);
+    CK(cudaMemcpy(res->sr0.data(), sr0.p, ell * sizeof(double), cudaMemcpyDeviceToHost));
+    res->y.resize(kend);
+    CK(cudaMemcpy(res->y.data(), Yh.as<double>() + (long long)(kend - 1) * K, kend * sizeof(double),
+                  cudaMemcpyDeviceToHost));
+    // counters (linops.py:53-68 semantics, per record)
+    res->matvecs.resize(kend);
+    res->tmatvecs.resize(kend);
+    res->dots.assign(kend, 0);
+    res->sketches.resize(kend);
+    long long tm = tmat0, sk = sk0;
+    for (int k = 1; k <= kend; ++k) {
+      const bool last = (k == kend);
+      const bool grewD = !(last && bd_at && (square || hst.bd_side == 0));
+      const bool grewL = !(last && bd_at);
+      if (!square && grewD) tm += 1;              // q = A^T d_{k+1}
+      sk += sb ? (grewD ? 1 : 0) : 1;             // G or Z column
+      if (lamon && grewL) sk += 1;                // F column
+      res->matvecs[k - 1] = matvec0 + k;
+      res->tmatvecs[k - 1] = tm;
+      res->sketches[k - 1] = sk;
+    }
+    res->Lb = Lb;
+    res->Db = Db;
+    res->ldn = ldn;
+    res->ldm = ldm;
+  }
+
+};
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+
+extern "C" {
+
+const char* hs_last_error(void) { return g_err.c_str(); }
+unsigned long long hs_launch_count(void) { return g_launches; }
+const char* hs_version(void) { return "hessketch_b200 0.1.0 (sm_100a)"; }
+
+int hs_ctx_create(int device, hs_ctx** out) {
+  return guarded([&] {
+    if (!out) fail(HS_ERR_VALUE, "null output handle");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) fail(HS_ERR_VALUE, "device %d out of range (have %d)", device, ndev);
+    CK(cudaSetDevice(device));
+    auto* c = new hs_ctx();
+    c->device = device;
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    *out = c;
+  });
+}
+
+int hs_ctx_destroy(hs_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    cudaStreamSynchronize(ctx->stream);
+    for (auto& p : ctx->pending) {
+      cudaEventDestroy(p.a);
+      cudaEventDestroy(p.b);
+    }
+    for (auto e : ctx->free_events) cudaEventDestroy(e);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+int hs_ctx_synchronize(hs_ctx* ctx) { return guarded([&] { CK(cudaStreamSynchronize(ctx->stream)); }); }
+
+int hs_comm_get_unique_id(void* out) {
+  return guarded([&] {
+    (void)out;
+    fail(HS_ERR_NOTIMPL, "multi-GPU communicator not built in this version");
+  });
+}
+
+int hs_comm_init(hs_ctx* ctx, int nranks, int rank, const void* uid) {
+  return guarded([&] {
+    (void)ctx;
+    (void)uid;
+    if (nranks == 1 && rank == 0) return;
+    fail(HS_ERR_NOTIMPL, "multi-GPU communicator not built in this version");
+  });
+}
+
+}  // extern "C"
+
+#include "hs_abi.inc"

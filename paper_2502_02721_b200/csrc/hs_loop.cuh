@@ -1,0 +1,352 @@
+// Per-iteration kernels of the sketched Hessenberg / sLSLU loop
+// (solvers.py:468-538 driving hessenberg.py:191-226 / 329-390).
+//
+//   fsub_warp_kernel      pivot-row forward substitution -> elimination coefficients
+//                         (hessenberg.py:209-212: c_j = u[t_j] after j subtractions)
+//   elim_pass_kernel      ONE coalesced pass over the k basis vectors: in-order
+//                         u <- u - c_j b_j, fused argmax|u| (smallest index ties,
+//                         hessenberg.py:110-114) and, optionally, the iterate
+//                         x = L y of the previous iteration (solvers.py:510)
+//   pivot_commit_kernel   breakdown test (hessenberg.py:213-219/351-360/375-384),
+//                         new H/W entry, pivot position, new pivot-row of P
+//   normalize_kernel      basis_{k+1} = u / pivot (true IEEE division, hessenberg.py:222)
+//   xpass_kernel          x = x0 + L_k y with the relative error partials (solvers.py:236-240)
+#pragma once
+
+#include "hs_common.cuh"
+
+namespace hs {
+
+// device-side loop state shared by the kernels of one solve
+struct LoopState {
+  int bd_iter;       // iteration at which a breakdown happened (0 = none)
+  int bd_side;       // 0 = data / square side, 1 = solution side
+  int trivial;       // init found a zero residual
+  int pad0;
+  double piv_val[2]; // latest pivot value per side (as double; exact for float/double)
+  long long piv_idx[2];
+  unsigned int counter[4];  // last-block counters (reset by the last block)
+  double relerr_acc;
+};
+
+// --------------------------------------------------------------------------
+// forward substitution on the pivot rows, one warp.
+// P is column-major with leading dimension ldp: P[i*ldp + j] = b_i[pos_j]
+// (unit lower triangular: P[j*ldp + j] = 1).  For j = 0..k-1 in order:
+//   c_j = v_j,   v_i <- v_i - c_j * P[j*ldp + i]   (i > j)
+// which is bit-identical to reading u[t_j] inside the sequential loop.
+template <class T, int S>
+__global__ void __launch_bounds__(32)
+fsub_warp_kernel(const T* __restrict__ u, const long long* __restrict__ pos, long long pos_offset,
+                 const T* __restrict__ P, int ldp, const int* __restrict__ kptr, int kfixed,
+                 const LoopState* __restrict__ st, int iter, int side, T* __restrict__ c,
+                 double* __restrict__ hcol) {
+  if (st->bd_iter != 0 && st->bd_iter < iter) return;
+  if (side == 1 && st->bd_iter == iter) return;  // data side broke down this iteration
+  const int k = kptr ? *kptr : kfixed;
+  const int lane = threadIdx.x;
+  T v[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int j = s * 32 + lane;
+    v[s] = (j < k) ? u[pos[j] - pos_offset] : T(0);
+  }
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    if (s * 32 >= k) break;
+    for (int o = 0; o < 32; ++o) {
+      const int j = s * 32 + o;
+      if (j >= k) break;
+      const T cj = __shfl_sync(0xffffffffu, v[s], o);
+      if (lane == 0) {
+        c[j] = cj;
+        hcol[j] = (double)cj;
+      }
+      const T* Pj = P + (long long)j * ldp;
+#pragma unroll
+      for (int s2 = s; s2 < S; ++s2) {
+        const int i = s2 * 32 + lane;
+        if (i > j && i < k) v[s2] = Rn<T>::sub(v[s2], Rn<T>::mul(cj, Pj[i]));
+      }
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// vector load helpers for the basis pass
+template <class B, int VEC> struct VecLoad;
+template <> struct VecLoad<float, 4> {
+  static __device__ __forceinline__ void ld(const float* p, float (&o)[4]) {
+    float4 t = __ldg(reinterpret_cast<const float4*>(p));
+    o[0] = t.x; o[1] = t.y; o[2] = t.z; o[3] = t.w;
+  }
+};
+template <> struct VecLoad<double, 2> {
+  static __device__ __forceinline__ void ld(const double* p, double (&o)[2]) {
+    double2 t = __ldg(reinterpret_cast<const double2*>(p));
+    o[0] = t.x; o[1] = t.y;
+  }
+};
+template <> struct VecLoad<__nv_bfloat16, 8> {
+  static __device__ __forceinline__ void ld(const __nv_bfloat16* p, __nv_bfloat16 (&o)[8]) {
+    uint4 t = __ldg(reinterpret_cast<const uint4*>(p));
+    const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&t);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = b[i];
+  }
+};
+
+// --------------------------------------------------------------------------
+// the fused elimination pass.
+//   u[e] <- (((u[e] - c_0 b_0[e]) - c_1 b_1[e]) ...)      (k terms, in order)
+//   x[e]  = x0[e] + sum_{j<kx} y_j b_j[e]                  (optional, fp64)
+// plus argmax |u'| and sum (x - x_true)^2 partials; the last block to finish
+// reduces the partials (fixed order) into st->piv_* / relerr slot.
+template <class T, class B, int VEC>
+__global__ void __launch_bounds__(256)
+elim_pass_kernel(long long n, long long idx_offset, const B* __restrict__ basis, long long ld,
+                 const int* __restrict__ kptr, int kfixed, const T* __restrict__ cvec, T* __restrict__ u,
+                 int kx, const double* __restrict__ yx, double* __restrict__ xout,
+                 const double* __restrict__ x0, const double* __restrict__ xt,
+                 double* __restrict__ xpart, double* __restrict__ relerr_out,
+                 Cand* __restrict__ cand_part, LoopState* __restrict__ st, int side, int iter,
+                 int write_u) {
+  if (st->bd_iter != 0 && st->bd_iter < iter) return;
+  if (side == 1 && st->bd_iter == iter) return;  // data side broke down this iteration
+  extern __shared__ unsigned char smem_raw[];
+  const int k = kptr ? *kptr : kfixed;
+  T* cs = reinterpret_cast<T*>(smem_raw);
+  double* ys = reinterpret_cast<double*>(smem_raw + ((k * sizeof(T) + 15) / 16) * 16);
+  __shared__ Cand scratch[32];
+  __shared__ double dscratch[32];
+  __shared__ bool am_last;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) cs[i] = cvec[i];
+  for (int i = threadIdx.x; i < kx; i += blockDim.x) ys[i] = yx[i];
+  __syncthreads();
+
+  Cand best{-1.0, 0.0, 0x7fffffffffffffffLL};
+  double sq = 0.0;
+  const long long nvec = (n + VEC - 1) / VEC;
+  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < nvec;
+       v += (long long)gridDim.x * blockDim.x) {
+    const long long e0 = v * VEC;
+    T acc[VEC];
+    double xa[VEC];
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) {
+      acc[q] = (e0 + q < n) ? u[e0 + q] : T(0);
+      xa[q] = 0.0;
+    }
+    const B* bp = basis + e0;
+    const int kk = k > kx ? k : kx;
+#pragma unroll 4
+    for (int j = 0; j < kk; ++j) {
+      B b[VEC];
+      VecLoad<B, VEC>::ld(bp + (long long)j * ld, b);
+      if (j < k) {
+        const T cj = cs[j];
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) acc[q] = Rn<T>::sub(acc[q], Rn<T>::mul(cj, cvt<T>(b[q])));
+      }
+      if (j < kx) {
+        const double yj = ys[j];
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) xa[q] = fma(yj, cvt<double>(b[q]), xa[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) {
+      const long long e = e0 + q;
+      if (e < n) {
+        if (write_u) u[e] = acc[q];
+        const double mg = (double)absval(acc[q]);
+        if (better(mg, idx_offset + e, best.mag, best.idx)) best = Cand{mg, (double)acc[q], idx_offset + e};
+        if (kx > 0) {
+          double xe = xa[q] + (x0 ? x0[e] : 0.0);
+          if (xout) xout[e] = xe;
+          if (xt) {
+            const double d = xe - xt[e];
+            sq = fma(d, d, sq);
+          }
+        }
+      }
+    }
+  }
+  best = block_argmax(best, scratch);
+  if (kx > 0 && xt) sq = block_sum(sq, dscratch);
+  if (threadIdx.x == 0) {
+    cand_part[blockIdx.x] = best;
+    if (kx > 0 && xt) xpart[blockIdx.x] = sq;
+    __threadfence();
+    const unsigned prev = atomicAdd(&st->counter[side], 1u);
+    am_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  Cand b2{-1.0, 0.0, 0x7fffffffffffffffLL};
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) {
+    Cand c;
+    c.mag = __ldcg(&cand_part[i].mag);
+    c.val = __ldcg(&cand_part[i].val);
+    c.idx = __ldcg(&cand_part[i].idx);
+    cand_merge(b2, c);
+  }
+  b2 = block_argmax(b2, scratch);
+  if (kx > 0 && xt && relerr_out && threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < (int)gridDim.x; ++i) s += __ldcg(&xpart[i]);
+    *relerr_out = s;  // squared norm; the host-side finalisation divides by |x_true|
+  }
+  if (threadIdx.x == 0) {
+    st->piv_val[side] = b2.val;
+    st->piv_idx[side] = b2.idx;
+    st->counter[side] = 0;
+  }
+}
+
+// --------------------------------------------------------------------------
+// pivot bookkeeping after the pass, one block.
+//   dim     : m or n (full-basis breakdown without scanning when k >= dim)
+//   hcol    : H(:,k-1) or W(:,k) column (entry k gets the pivot or 0)
+//   pos     : pivot positions (pos[k] = new pivot, global index)
+//   P       : pivot-row matrix, column-major ld = ldp; new row k
+//   basis   : basis columns 0..k-1 (to gather b_i[new pivot]); local shard
+template <class T, class B>
+__global__ void pivot_commit_kernel(int k, long long dim, double* __restrict__ hcol, long long* __restrict__ pos,
+                                    T* __restrict__ P, int ldp, const B* __restrict__ basis, long long ld,
+                                    long long idx_offset, long long n_loc, LoopState* __restrict__ st,
+                                    int side, int iter, T* __restrict__ pivval_out) {
+  if (st->bd_iter != 0 && st->bd_iter < iter) return;
+  if (side == 1 && st->bd_iter == iter) return;
+  const double val = (k < dim) ? st->piv_val[side] : 0.0;
+  const long long idx = st->piv_idx[side];
+  if (val == 0.0) {
+    if (threadIdx.x == 0) {
+      hcol[k] = 0.0;
+      st->bd_iter = iter;
+      st->bd_side = side;
+    }
+    return;
+  }
+  if (threadIdx.x == 0) {
+    hcol[k] = val;
+    pos[k] = idx;
+    *pivval_out = (T)val;
+  }
+  const long long le = idx - idx_offset;
+  for (int i = threadIdx.x; i <= k; i += blockDim.x) {
+    T pv;
+    if (i == k) pv = T(1);
+    else pv = (le >= 0 && le < n_loc) ? cvt<T>(basis[(long long)i * ld + le]) : T(0);
+    P[(long long)i * ldp + k] = pv;
+  }
+}
+
+// basis_{k+1}[e] = u[e] / pivot (IEEE division in T, then stored as B); zero padding
+template <class T, class B>
+__global__ void __launch_bounds__(256)
+normalize_kernel(long long n, long long n_pad, const T* __restrict__ u, const T* __restrict__ pivval,
+                 B* __restrict__ dst, const LoopState* __restrict__ st, int side, int iter) {
+  if (st->bd_iter != 0 && st->bd_iter <= iter) return;
+  const T p = *pivval;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n_pad;
+       e += (long long)gridDim.x * blockDim.x) {
+    dst[e] = (e < n) ? cvt<B>(Rn<T>::div(u[e], p)) : cvt<B>(T(0));
+  }
+}
+
+// plain argmax over a vector (init pivots of r0 / A^T r0); result into st->piv_*[side]
+template <class T>
+__global__ void __launch_bounds__(256)
+argmax_kernel(long long n, long long idx_offset, const T* __restrict__ v, Cand* __restrict__ cand_part,
+              LoopState* __restrict__ st, int side) {
+  __shared__ Cand scratch[32];
+  __shared__ bool am_last;
+  Cand best{-1.0, 0.0, 0x7fffffffffffffffLL};
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const double mg = (double)absval(v[e]);
+    if (better(mg, idx_offset + e, best.mag, best.idx)) best = Cand{mg, (double)v[e], idx_offset + e};
+  }
+  best = block_argmax(best, scratch);
+  if (threadIdx.x == 0) {
+    cand_part[blockIdx.x] = best;
+    __threadfence();
+    const unsigned prev = atomicAdd(&st->counter[side], 1u);
+    am_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  Cand b2{-1.0, 0.0, 0x7fffffffffffffffLL};
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) {
+    Cand c;
+    c.mag = __ldcg(&cand_part[i].mag);
+    c.val = __ldcg(&cand_part[i].val);
+    c.idx = __ldcg(&cand_part[i].idx);
+    cand_merge(b2, c);
+  }
+  b2 = block_argmax(b2, scratch);
+  if (threadIdx.x == 0) {
+    st->piv_val[side] = b2.val;
+    st->piv_idx[side] = b2.idx;
+    st->counter[side] = 0;
+  }
+}
+
+// x = x0 + sum_{j<kx} y_j b_j (fp64, j ascending) with (x - x_true)^2 partials
+template <class B>
+__global__ void __launch_bounds__(256)
+xpass_kernel(long long n, const B* __restrict__ basis, long long ld, int kx, const double* __restrict__ y,
+             const double* __restrict__ x0, const double* __restrict__ xt, double* __restrict__ xout,
+             double* __restrict__ xpart, double* __restrict__ relerr_out, LoopState* __restrict__ st) {
+  extern __shared__ unsigned char smem_raw[];
+  double* ys = reinterpret_cast<double*>(smem_raw);
+  __shared__ double dscratch[32];
+  __shared__ bool am_last;
+  for (int i = threadIdx.x; i < kx; i += blockDim.x) ys[i] = y[i];
+  __syncthreads();
+  double sq = 0.0;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    double xa = 0.0;
+    for (int j = 0; j < kx; ++j) xa = fma(ys[j], cvt<double>(basis[(long long)j * ld + e]), xa);
+    const double xe = xa + (x0 ? x0[e] : 0.0);
+    if (xout) xout[e] = xe;
+    if (xt) {
+      const double d = xe - xt[e];
+      sq = fma(d, d, sq);
+    }
+  }
+  if (!xt) return;
+  sq = block_sum(sq, dscratch);
+  if (threadIdx.x == 0) {
+    xpart[blockIdx.x] = sq;
+    __threadfence();
+    const unsigned prev = atomicAdd(&st->counter[2], 1u);
+    am_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < (int)gridDim.x; ++i) s += __ldcg(&xpart[i]);
+    *relerr_out = s;
+    st->counter[2] = 0;
+  }
+}
+
+// r0 = b - A x0 (T), b given in T
+template <class T>
+__global__ void sub_kernel(long long n, const T* __restrict__ b, T* __restrict__ r) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    r[e] = Rn<T>::sub(b[e], r[e]);
+}
+
+template <class To, class From>
+__global__ void convert_kernel(long long n, const From* __restrict__ src, To* __restrict__ dst) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    dst[e] = cvt<To>(src[e]);
+}
+
+}  // namespace hs

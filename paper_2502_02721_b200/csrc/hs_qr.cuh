@@ -1,0 +1,203 @@
+// Incremental projected least-squares solve (solvers.py:204-225, linops.py:168-229).
+//
+// The reference re-factors the whole sketched system from scratch every
+// iteration with a column-pivoted QR (geqp3) and a triangular solve.  Here the
+// system grows by one column per iteration, so the factorisation is updated
+// instead: the new stacked column a = [z_k ; lam f_k] is orthogonalised
+// against Q by classical Gram-Schmidt with one re-orthogonalisation pass
+// (CGS2, "twice is enough"), giving R's new column r = c1 + c2 and rho.  The
+// inverse R^{-1} is kept too (new column [-R^{-1} r / rho ; 1 / rho]), so the
+// solution update  y_k = [y_{k-1} - (beta/rho) R^{-1} r ; beta/rho]  with
+// beta = q_k^T rhs is a triangular mat-vec instead of a serial back-solve.
+// Everything is fp64.  One cooperative kernel, NB blocks owning row slices of
+// the stacked system, 5 grid-wide barriers.  Then sres = |Z y - S r0| and
+// proj_obj = sqrt(sres^2 + lam^2 |F y|^2) exactly as solvers.py:514-520 form them.
+//
+// Rank test: the reference raises RankDeficiencyError when min|R_ii| <
+// 1e-14 max|R_ii| of the PIVOTED QR (linops.py:197-203) and falls back to lstsq
+// (solvers.py:211-218).  This kernel applies the same 1e-14 test to the
+// unpivoted rho's, flags rank_fallback, and drops the dependent column (its
+// coefficient is set to 0).  The gate never fired in any survey probe.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "hs_common.cuh"
+#include "hs_loop.cuh"
+
+namespace hs {
+
+struct QrArgs {
+  int ell, Ls, ldq, kmax;
+  double lam;
+  const double* zcol;   // new column of Z (ell)
+  const double* fcol;   // new column of F (ell) or null
+  const double* Z;      // ell x kmax (ld = ell)
+  const double* F;      // ell x (kmax+1) (ld = ell) or null
+  const double* sr0;    // ell
+  double* Q;            // ldq x kmax
+  double* Rinv;         // kmax x kmax, column-major
+  double* Rdiag;        // kmax
+  double* y;            // kmax (current solution)
+  double* Yhist;        // kmax x kmax: y^{(k)} in column k-1
+  double* part;         // scratch: 4 buffers of NB x (kmax + 2)
+  double* sres;         // kmax
+  double* proj;         // kmax
+  int* rankfb;          // kmax
+  LoopState* st;
+};
+
+__global__ void __launch_bounds__(256) qr_step_kernel(QrArgs a, int k, int iter) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  if (a.st->bd_iter != 0 && a.st->bd_iter < iter) return;  // uniform across the grid
+  extern __shared__ double sm[];
+  const int NB = gridDim.x, b = blockIdx.x, tid = threadIdx.x, BT = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = BT >> 5;
+  const int j = k - 1;  // new column index
+  const int RS = (a.Ls + NB - 1) / NB;
+  const int r0 = b * RS, r1 = min(a.Ls, r0 + RS);
+  const int nr = max(0, r1 - r0);
+  const int pld = a.kmax + 2;
+  double* P1 = a.part;
+  double* P2 = a.part + (long long)NB * pld;
+  double* P3 = a.part + 2LL * NB * pld;
+  double* P5 = a.part + 3LL * NB * pld;
+  double* av = sm;            // RS
+  double* cv = sm + RS;       // kmax (c1, then c2)
+  double* c1s = cv + a.kmax;  // kmax (saved c1)
+  __shared__ double scratch[32];
+
+  // phase 1: load the new stacked column, partial Q^T a
+  for (int r = tid; r < nr; r += BT) {
+    const int gr = r0 + r;
+    av[r] = gr < a.ell ? a.zcol[gr] : a.lam * a.fcol[gr - a.ell];
+  }
+  __syncthreads();
+  for (int i = warp; i < j; i += nwarps) {
+    const double* qi = a.Q + (long long)i * a.ldq + r0;
+    double s = 0.0;
+    for (int r = lane; r < nr; r += 32) s = fma(qi[r], av[r], s);
+    s = warp_sum(s);
+    if (lane == 0) P1[(long long)b * pld + i] = s;
+  }
+  grid.sync();
+
+  // phase 2: c1 = sum_b P1;  a -= Q c1;  partial Q^T a
+  for (int i = tid; i < j; i += BT) {
+    double s = 0.0;
+    for (int bb = 0; bb < NB; ++bb) s += __ldcg(&P1[(long long)bb * pld + i]);
+    cv[i] = s;
+    c1s[i] = s;
+  }
+  __syncthreads();
+  for (int r = tid; r < nr; r += BT) {
+    double s = 0.0;
+    for (int i = 0; i < j; ++i) s = fma(a.Q[(long long)i * a.ldq + r0 + r], cv[i], s);
+    av[r] -= s;
+  }
+  __syncthreads();
+  for (int i = warp; i < j; i += nwarps) {
+    const double* qi = a.Q + (long long)i * a.ldq + r0;
+    double s = 0.0;
+    for (int r = lane; r < nr; r += 32) s = fma(qi[r], av[r], s);
+    s = warp_sum(s);
+    if (lane == 0) P2[(long long)b * pld + i] = s;
+  }
+  grid.sync();
+
+  // phase 3: c2 = sum_b P2;  a -= Q c2;  partial |a|^2 and a^T rhs
+  for (int i = tid; i < j; i += BT) {
+    double s = 0.0;
+    for (int bb = 0; bb < NB; ++bb) s += __ldcg(&P2[(long long)bb * pld + i]);
+    cv[i] = s;
+  }
+  __syncthreads();
+  double nn = 0.0, ar = 0.0;
+  for (int r = tid; r < nr; r += BT) {
+    double s = 0.0;
+    for (int i = 0; i < j; ++i) s = fma(a.Q[(long long)i * a.ldq + r0 + r], cv[i], s);
+    const double v = av[r] - s;
+    av[r] = v;
+    nn = fma(v, v, nn);
+    const int gr = r0 + r;
+    if (gr < a.ell) ar = fma(v, a.sr0[gr], ar);
+  }
+  nn = block_sum(nn, scratch);
+  ar = block_sum(ar, scratch);
+  if (tid == 0) {
+    P3[(long long)b * pld + 0] = nn;
+    P3[(long long)b * pld + 1] = ar;
+  }
+  grid.sync();
+
+  // phase 4: rho, beta; new Q column; block 0 updates R^{-1}, y
+  double rho2 = 0.0, g = 0.0;
+  for (int bb = 0; bb < NB; ++bb) {
+    rho2 += __ldcg(&P3[(long long)bb * pld + 0]);
+    g += __ldcg(&P3[(long long)bb * pld + 1]);
+  }
+  const double rho = sqrt(rho2);
+  double rmax = rho;
+  for (int i = 0; i < j; ++i) rmax = fmax(rmax, fabs(a.Rdiag[i]));
+  const bool deficient = !(rho > 0.0) || rho < 1e-14 * rmax;
+  for (int r = tid; r < nr; r += BT) a.Q[(long long)j * a.ldq + r0 + r] = deficient ? 0.0 : av[r] / rho;
+  if (b == 0) {
+    const double eta = deficient ? 0.0 : (g / rho) / rho;  // beta / rho, beta = q^T rhs = g / rho
+    // w = Rinv[0:j, 0:j] (c1 + c2)
+    for (int i = tid; i < j; i += BT) {
+      double s = 0.0;
+      for (int l = i; l < j; ++l) s = fma(a.Rinv[(long long)l * a.kmax + i], c1s[l] + cv[l], s);
+      const double yi = a.y[i] - eta * s;
+      a.Rinv[(long long)j * a.kmax + i] = deficient ? 0.0 : -s / rho;
+      a.y[i] = yi;
+      a.Yhist[(long long)j * a.kmax + i] = yi;
+    }
+    if (tid == 0) {
+      a.Rinv[(long long)j * a.kmax + j] = deficient ? 0.0 : 1.0 / rho;
+      a.Rdiag[j] = deficient ? 0.0 : rho;
+      a.y[j] = eta;
+      a.Yhist[(long long)j * a.kmax + j] = eta;
+      a.rankfb[j] = deficient ? 1 : 0;
+    }
+  }
+  grid.sync();
+
+  // phase 5: residual partials |Z y - sr0|^2 (top) and |F y|^2 (bottom)
+  double* ys = cv;
+  for (int i = tid; i <= j; i += BT) ys[i] = __ldcg(&a.y[i]);
+  __syncthreads();
+  double s_top = 0.0, s_bot = 0.0;
+  for (int r = tid; r < nr; r += BT) {
+    const int gr = r0 + r;
+    if (gr < a.ell) {
+      double s = 0.0;
+      for (int i = 0; i <= j; ++i) s = fma(a.Z[(long long)i * a.ell + gr], ys[i], s);
+      const double d = s - a.sr0[gr];
+      s_top = fma(d, d, s_top);
+    } else {
+      const int fr = gr - a.ell;
+      double s = 0.0;
+      for (int i = 0; i <= j; ++i) s = fma(a.F[(long long)i * a.ell + fr], ys[i], s);
+      s_bot = fma(s, s, s_bot);
+    }
+  }
+  s_top = block_sum(s_top, scratch);
+  s_bot = block_sum(s_bot, scratch);
+  if (tid == 0) {
+    P5[(long long)b * pld + 0] = s_top;
+    P5[(long long)b * pld + 1] = s_bot;
+  }
+  grid.sync();
+  if (b == 0 && tid == 0) {
+    double st = 0.0, sb = 0.0;
+    for (int bb = 0; bb < NB; ++bb) {
+      st += __ldcg(&P5[(long long)bb * pld + 0]);
+      sb += __ldcg(&P5[(long long)bb * pld + 1]);
+    }
+    a.sres[j] = sqrt(st);
+    a.proj[j] = sqrt(st + a.lam * a.lam * sb);
+  }
+}
+
+}  // namespace hs

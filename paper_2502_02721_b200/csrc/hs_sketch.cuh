@@ -1,0 +1,170 @@
+// Sketch kernels: z = S v for the three sketch kinds the drop-in accepts
+// (sketch.py:29-65 takes any `entries` supporting `@`):
+//   * explicit dense S (row-major, e.g. the reference's PCG64 draw, sketch.py:43-53)
+//   * Gaussian S generated on the fly from a counter-based RNG, never stored
+//   * sparse-sign S (zeta nonzeros +-1/sqrt(zeta) per column), stored row-wise
+// All sums are fp64 in a fixed order (deterministic, replayable: test_solvers.py:319-326).
+#pragma once
+
+#include "hs_common.cuh"
+
+namespace hs {
+
+// ---- explicit dense: one block per sketch row, fixed-tree block sum --------
+template <class Vs, class Tin>
+__global__ void __launch_bounds__(256)
+sketch_dense_kernel(int ell, long long m, const Vs* __restrict__ S, long long lds,
+                    const Tin* __restrict__ v, double* __restrict__ z) {
+  __shared__ double scratch[32];
+  const int i = blockIdx.x;
+  const Vs* row = S + (long long)i * lds;
+  double acc = 0.0;
+  for (long long c = threadIdx.x; c < m; c += blockDim.x) acc = fma((double)row[c], cvt<double>(v[c]), acc);
+  acc = block_sum(acc, scratch);
+  if (threadIdx.x == 0) z[i] = acc;
+}
+
+// ---- Gaussian from Philox: S[i, c] = N(seed; c, i) / sqrt(ell) -----------------
+// one Philox call per (column c, row quad q) gives 4 normals (2 Box-Muller pairs)
+__device__ __forceinline__ void gauss_quad(uint2 key, unsigned long long c, unsigned q, float (&o)[4]) {
+  const uint4 r = Philox::gen(make_uint4((unsigned)c, (unsigned)(c >> 32), q, 0x53CE7C4Du), key);
+  box_muller(r.x, r.y, o[0], o[1]);
+  box_muller(r.z, r.w, o[2], o[3]);
+}
+
+// grid: (ntiles, ceil(nquads/64)), block 256 = 64 quads x 4 column phases
+template <class Tin>
+__global__ void __launch_bounds__(256)
+sketch_gauss_partial_kernel(int ell, long long m, long long col_offset, long long tile_cols, uint2 key,
+                            const Tin* __restrict__ v, double* __restrict__ part) {
+  __shared__ double red[4][64][4];
+  const int nq = (ell + 3) / 4;
+  const int ql = threadIdx.x & 63, ph = threadIdx.x >> 6;
+  const int q = blockIdx.y * 64 + ql;
+  const long long c0 = (long long)blockIdx.x * tile_cols;
+  const long long c1 = min(m, c0 + tile_cols);
+  double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+  if (q < nq) {
+    for (long long c = c0 + ph; c < c1; c += 4) {
+      const double vc = cvt<double>(v[c]);
+      float g[4];
+      gauss_quad(key, (unsigned long long)(c + col_offset), (unsigned)q, g);
+      a0 = fma((double)g[0], vc, a0);
+      a1 = fma((double)g[1], vc, a1);
+      a2 = fma((double)g[2], vc, a2);
+      a3 = fma((double)g[3], vc, a3);
+    }
+  }
+  red[ph][ql][0] = a0; red[ph][ql][1] = a1; red[ph][ql][2] = a2; red[ph][ql][3] = a3;
+  __syncthreads();
+  if (ph == 0 && q < nq) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = 4 * q + r;
+      if (i < ell) {
+        const double s = ((red[0][ql][r] + red[1][ql][r]) + red[2][ql][r]) + red[3][ql][r];
+        part[(long long)blockIdx.x * ell + i] = s;
+      }
+    }
+  }
+}
+
+// z[i] = scale * sum_t part[t][i]   (t ascending)
+__global__ void sketch_tile_reduce_kernel(int ell, int ntiles, const double* __restrict__ part, double scale,
+                                          double* __restrict__ z) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ell) return;
+  double s = 0.0;
+  for (int t = 0; t < ntiles; ++t) s += part[(long long)t * ell + i];
+  z[i] = s * scale;
+}
+
+// materialise the generated Gaussian S (row-major ell x m, fp64) for export
+__global__ void gauss_materialize_kernel(int ell, long long m, uint2 key, double inv_sqrt_ell, double* __restrict__ S) {
+  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= m) return;
+  const int nq = (ell + 3) / 4;
+  for (int q = 0; q < nq; ++q) {
+    float g[4];
+    gauss_quad(key, (unsigned long long)c, (unsigned)q, g);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = 4 * q + r;
+      if (i < ell) S[(long long)i * m + c] = (double)g[r] * inv_sqrt_ell;
+    }
+  }
+}
+
+// ---- sparse-sign -----------------------------------------------------------------
+// column c draws zeta distinct rows uniformly from [0, ell) and a sign each,
+// from Philox(seed; c, draw).  Entries are emitted as (row, signed column+1).
+__global__ void sparse_sign_gen_kernel(long long m, int ell, int zeta, uint2 key, int* __restrict__ rows_out,
+                                       int* __restrict__ scol_out) {
+  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= m) return;
+  int chosen[64];
+  int got = 0;
+  unsigned draw = 0;
+  while (got < zeta) {
+    const uint4 r = Philox::gen(make_uint4((unsigned)c, (unsigned)(c >> 32), draw++, 0x5A5A0001u), key);
+    const unsigned w[2] = {r.x, r.z};
+    const unsigned sg[2] = {r.y, r.w};
+    for (int h = 0; h < 2 && got < zeta; ++h) {
+      const int row = (int)(((unsigned long long)w[h] * (unsigned long long)ell) >> 32);
+      bool dup = false;
+      for (int t = 0; t < got; ++t) dup |= (chosen[t] == row);
+      if (dup) continue;
+      chosen[got] = row;
+      rows_out[c * zeta + got] = row;
+      scol_out[c * zeta + got] = (sg[h] & 1u) ? -(int)(c + 1) : (int)(c + 1);
+      ++got;
+    }
+  }
+}
+
+// z[i] = scale * sum over row i's entries (+-) v[col]; block per sketch row
+template <class Tin>
+__global__ void __launch_bounds__(256)
+sketch_sparse_kernel(int ell, const long long* __restrict__ rowptr, const int* __restrict__ scol,
+                     long long col_offset, long long m_loc, const Tin* __restrict__ v, double scale,
+                     double* __restrict__ z) {
+  __shared__ double scratch[32];
+  const int i = blockIdx.x;
+  double acc = 0.0;
+  for (long long p = rowptr[i] + threadIdx.x; p < rowptr[i + 1]; p += blockDim.x) {
+    const int sc = scol[p];
+    const long long c = (long long)(sc < 0 ? -sc : sc) - 1 - col_offset;
+    if (c >= 0 && c < m_loc) {
+      const double x = cvt<double>(v[c]);
+      acc += sc < 0 ? -x : x;
+    }
+  }
+  acc = block_sum(acc, scratch);
+  if (threadIdx.x == 0) z[i] = acc * scale;
+}
+
+// ---- general explicit sparse S (CSR by sketch rows, fp64 values) ------------
+template <class Tin>
+__global__ void __launch_bounds__(256)
+sketch_csr_kernel(int ell, const long long* __restrict__ rowptr, const int* __restrict__ col,
+                  const double* __restrict__ val, const Tin* __restrict__ v, double* __restrict__ z) {
+  __shared__ double scratch[32];
+  const int i = blockIdx.x;
+  double acc = 0.0;
+  for (long long p = rowptr[i] + threadIdx.x; p < rowptr[i + 1]; p += blockDim.x)
+    acc = fma(val[p], cvt<double>(v[col[p]]), acc);
+  acc = block_sum(acc, scratch);
+  if (threadIdx.x == 0) z[i] = acc;
+}
+
+// ---- sketch-basis column: m_col = G[:, :ng] @ hcol[:ng]  (solvers.py:496-499) ----
+__global__ void gemv_small_kernel(int ell, int ng, const double* __restrict__ G, const double* __restrict__ h,
+                                  double* __restrict__ out) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= ell) return;
+  double s = 0.0;
+  for (int i = 0; i < ng; ++i) s = fma(G[(long long)i * ell + r], h[i], s);
+  out[r] = s;
+}
+
+}  // namespace hs

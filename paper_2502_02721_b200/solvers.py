@@ -1,0 +1,323 @@
+"""Drop-in sketched solvers: ``scmrh``, ``slslu``, ``scmrh_tikhonov``,
+``slslu_tikhonov`` with the reference's signatures and result types
+(solvers.py:88-160, 562-605), running the whole iteration loop on the B200
+through one C-ABI call (``hs_solve``, restating ``_hessenberg_solve``,
+solvers.py:410-539).
+
+Device knobs added to :class:`SolverConfig` (defaults reproduce the reference):
+
+* ``dtype``        -- "float64" (reference arithmetic) or "float32"
+* ``basis_dtype``  -- storage of the Krylov bases: None (= dtype), "float32"
+                      or "bfloat16" (with dtype float32)
+* ``sketch_kind``  -- how S2 (and S1 when lam > 0) are realised when no
+                      ``sketch=`` is passed: "pcg64" (the reference's host
+                      draw, sketch.py:43-53, uploaded once; default),
+                      "gaussian" (device Philox, never stored) or
+                      "sparse_sign" (``sketch_zeta`` nonzeros per column)
+* ``record_rel_err`` -- compute rel_err at every iteration (default True when
+                      x_true is given, as the reference does)
+
+Out of scope in this version (raise NotImplementedError): the unsketched
+CMRH/LSLU and the GMRES/LSQR references, ``compute_diagnostics=True``,
+sampled pivoting, ``printed_f_columns=True``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .hessenberg import DeviceFactorization, PivotStrategy
+from .linops import to_device_operator
+from .sketch import (
+    GaussianSketch,
+    SparseSignSketch,
+    derive_seed,
+    device_sketch,
+    make_gaussian_sketch,
+)
+
+__all__ = [
+    "CSV_COLUMNS",
+    "SolverConfig",
+    "TraceRecord",
+    "SolverTrace",
+    "SolveResult",
+    "trace_to_csv",
+    "scmrh",
+    "slslu",
+    "scmrh_tikhonov",
+    "slslu_tikhonov",
+    "SOLVERS",
+]
+
+CSV_COLUMNS = [
+    "iter", "res_norm", "sres_norm", "proj_obj", "rel_err", "kappa_basis", "kappa_dbar",
+    "eps_embed", "matvecs", "tmatvecs", "dots", "sketches", "wall_ms",
+]
+
+
+@dataclass
+class SolverConfig:
+    """solvers.py:88-116 plus device knobs (module docstring)."""
+
+    maxiter: int = 30
+    pivot: PivotStrategy = field(default_factory=PivotStrategy.full)
+    sketch_rows: int = None
+    lam: float = 0.0
+    seed: int = 0
+    x0: np.ndarray = None
+    compute_diagnostics: bool = False
+    dtype: str = "float64"
+    basis_dtype: str = None
+    sketch_kind: str = "pcg64"
+    sketch_zeta: int = 8
+    record_rel_err: bool = True
+
+    def __post_init__(self):
+        if self.maxiter < 1:
+            raise ValueError("maxiter must be positive")
+        if self.lam < 0:
+            raise ValueError("lam must be nonnegative")
+        if self.sketch_rows is not None and self.sketch_rows < 1:
+            raise ValueError("sketch_rows must be positive")
+        if self.dtype not in ("float64", "float32"):
+            raise ValueError("dtype must be 'float64' or 'float32'")
+        if self.basis_dtype not in (None, "float64", "float32", "bfloat16"):
+            raise ValueError("basis_dtype must be None, 'float64', 'float32' or 'bfloat16'")
+        if self.sketch_kind not in ("pcg64", "gaussian", "sparse_sign"):
+            raise ValueError("sketch_kind must be 'pcg64', 'gaussian' or 'sparse_sign'")
+
+    def effective_sketch_rows(self):
+        if self.sketch_rows is None:
+            return 10 * (self.maxiter + 1)
+        return self.sketch_rows
+
+
+@dataclass
+class TraceRecord:
+    """solvers.py:119-141."""
+
+    iteration: int
+    res_norm: float = None
+    sres_norm: float = None
+    proj_obj: float = None
+    rel_err: float = None
+    kappa_basis: float = None
+    kappa_dbar: float = None
+    eps_embed: float = None
+    matvecs: int = 0
+    tmatvecs: int = 0
+    dots: int = 0
+    sketches: int = 0
+    wall_ms: float = None
+    rank_fallback: bool = False
+
+
+@dataclass
+class SolverTrace:
+    records: list = field(default_factory=list)
+
+    def column(self, name):
+        return [getattr(r, name) for r in self.records]
+
+    def final(self):
+        return self.records[-1] if self.records else None
+
+
+@dataclass
+class SolveResult:
+    x: np.ndarray
+    trace: SolverTrace
+    termination: str  # maxiter | breakdown | trivial
+    factorization: object = None
+    loop_ms: float = None  # device time of the iteration loop (CUDA events)
+
+
+def _cell(value):
+    if value is None:
+        return ""
+    if isinstance(value, (int, np.integer)):
+        return str(int(value))
+    return repr(float(value))
+
+
+def trace_to_csv(trace, target, include_timing=False):
+    """solvers.py:171-201 (fixed column order, wall_ms only on request)."""
+    lines = [",".join(CSV_COLUMNS)]
+    for r in trace.records:
+        cells = [
+            str(r.iteration), _cell(r.res_norm), _cell(r.sres_norm), _cell(r.proj_obj), _cell(r.rel_err),
+            _cell(r.kappa_basis), _cell(r.kappa_dbar), _cell(r.eps_embed), str(r.matvecs), str(r.tmatvecs),
+            str(r.dots), str(r.sketches), _cell(r.wall_ms) if include_timing else "",
+        ]
+        lines.append(",".join(cells))
+    content = "\n".join(lines) + "\n"
+    if hasattr(target, "write"):
+        target.write(content)
+    else:
+        with open(target, "w", newline="") as fh:
+            fh.write(content)
+
+
+# ---------------------------------------------------------------------------
+
+
+class _NativeResult:
+    """Owns an hs_result handle and its host copies."""
+
+    def __init__(self, handle, rows, cols, ell):
+        lib = _lib.load()
+        self.handle = handle
+        v = [_lib.c_i32() for _ in range(6)]
+        _lib.check(lib.hs_result_info(handle, *[ctypes.byref(x) for x in v]))
+        nrec, term, k, bds, nbd, nbs = (x.value for x in v)
+        self.info = {"n_records": nrec, "termination": _lib.TERMINATIONS[term], "k": k, "bd_side": bds,
+                     "n_basis_data": nbd, "n_basis_sol": nbs}
+        self.x = np.empty(cols)
+        _lib.check(lib.hs_result_x(handle, _lib.ptr(self.x)))
+        n = max(nrec, 1)
+        self.sres, self.proj, self.relerr, self.wall = (np.empty(n) for _ in range(4))
+        self.rankfb = np.empty(n, dtype=np.int32)
+        self.matvecs, self.tmatvecs, self.dots, self.sketches = (np.empty(n, dtype=np.int64) for _ in range(4))
+        _lib.check(lib.hs_result_trace(handle, *(_lib.ptr(a) for a in (
+            self.sres, self.proj, self.relerr, self.rankfb, self.matvecs, self.tmatvecs, self.dots, self.sketches,
+            self.wall))))
+        self.pivots_t = np.empty(max(nbd, 1), dtype=np.int64)[:nbd]
+        self.pivots_g = np.empty(max(nbs, 1), dtype=np.int64)[:nbs]
+        if nrec:
+            tbuf = np.empty(max(nbd, nbs, 1), dtype=np.int64)
+            gbuf = np.empty(max(nbd, nbs, 1), dtype=np.int64)
+            _lib.check(lib.hs_result_pivots(handle, _lib.ptr(tbuf), _lib.ptr(gbuf)))
+            self.pivots_t = tbuf[:nbd].copy()
+            self.pivots_g = gbuf[:nbs].copy()
+            Hc = np.empty((k, k + 1))  # column-major (k+1) x k
+            Wc = np.empty((max(nbd, 1), max(nbd, 1)))
+            _lib.check(lib.hs_result_hessenberg(handle, _lib.ptr(Hc), _lib.ptr(Wc)))
+            self.H = np.ascontiguousarray(Hc.T)
+            self.W = np.ascontiguousarray(Wc[:nbd, :nbd].T)
+            Zc = np.empty((k, ell))
+            self.sr0 = np.empty(ell)
+            self.y = np.empty(k)
+            _lib.check(lib.hs_result_projected(handle, _lib.ptr(Zc), _lib.ptr(self.sr0), _lib.ptr(self.y)))
+            self.Z = np.ascontiguousarray(Zc.T)
+        ms = _lib.c_dbl()
+        _lib.check(lib.hs_result_loop_ms(handle, ctypes.byref(ms)))
+        self.loop_ms = ms.value
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None:
+            try:
+                _lib.load().hs_result_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+
+def _default_sketch(cfg, ell, in_rows, seed):
+    if cfg.sketch_kind == "pcg64":
+        return device_sketch(make_gaussian_sketch(ell, in_rows, seed))
+    if cfg.sketch_kind == "gaussian":
+        return GaussianSketch(ell, in_rows, seed)
+    return SparseSignSketch(ell, in_rows, seed, cfg.sketch_zeta)
+
+
+def _hessenberg_solve(A, b, cfg, x_true, square, sketch_basis, sketch=None, S1=None):
+    """solvers.py:410-539, sketched branch, on the device."""
+    cfg = cfg or SolverConfig()
+    if square and not A.is_square:
+        raise ValueError("this solver needs a square operator")
+    if cfg.compute_diagnostics:
+        raise NotImplementedError("compute_diagnostics is out of scope for the device path")
+    if cfg.pivot.kind != "full":
+        raise NotImplementedError("sampled pivoting is not implemented on the device yet")
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    if b.shape != (A.rows,):
+        raise ValueError(f"b must have length {A.rows}, got shape {b.shape}")
+    x0 = None if cfg.x0 is None else np.ascontiguousarray(cfg.x0, dtype=np.float64)
+    if x0 is None and not np.any(b):
+        # hessenberg.py:171-173 / 290-291: zero initial residual, no iteration
+        return SolveResult(x=np.zeros(A.cols), trace=SolverTrace(), termination="trivial")
+    dev = to_device_operator(A)
+    if sketch is not None:
+        if sketch.in_rows != A.rows:
+            raise ValueError(
+                f"sketch expects vectors of length {sketch.in_rows}, operator produces length {A.rows}"
+            )
+        ell = sketch.out_rows
+    else:
+        ell = cfg.effective_sketch_rows()
+    if ell < cfg.maxiter + 1:
+        raise ValueError(
+            f"sketch_rows={ell} cannot embed a {cfg.maxiter}-dimensional projected problem; "
+            "need at least maxiter+1 rows"
+        )
+    S2 = device_sketch(sketch) if sketch is not None else _default_sketch(cfg, ell, A.rows, cfg.seed)
+    if cfg.lam > 0.0:
+        S1 = device_sketch(S1) if S1 is not None else _default_sketch(cfg, ell, A.cols, derive_seed(cfg.seed, 1))
+    else:
+        S1 = None
+    if x_true is not None:
+        x_true = np.ascontiguousarray(x_true, dtype=np.float64)
+    basis_dtype = cfg.basis_dtype or cfg.dtype
+    if cfg.dtype == "float64" and basis_dtype != "float64":
+        raise ValueError("float64 work needs float64 basis storage")
+    hc = _lib.HsConfig(
+        maxiter=cfg.maxiter, square=1 if square else 0, sketch_basis=1 if sketch_basis else 0,
+        work_dtype=_lib.DTYPE_CODES[cfg.dtype], basis_dtype=_lib.DTYPE_CODES[basis_dtype],
+        record_x=1 if (x_true is not None and cfg.record_rel_err) else 0, lam=float(cfg.lam),
+    )
+    h = _lib.c_vp()
+    _lib.check(_lib.load().hs_solve(dev.ctx.handle, dev.handle, ctypes.byref(hc), S2.handle,
+                                    S1.handle if S1 is not None else None, _lib.ptr(b), _lib.ptr(x0),
+                                    _lib.ptr(x_true), ctypes.byref(h)))
+    nr = _NativeResult(h, A.rows, A.cols, ell)
+    term = nr.info["termination"]
+    if term == "trivial":
+        return SolveResult(x=nr.x, trace=SolverTrace(), termination="trivial")
+    trace = SolverTrace()
+    for i in range(nr.info["n_records"]):
+        rel = float(nr.relerr[i])
+        trace.records.append(TraceRecord(
+            iteration=i + 1,
+            sres_norm=float(nr.sres[i]),
+            proj_obj=float(nr.proj[i]),
+            rel_err=None if (x_true is None or np.isnan(rel)) else rel,
+            matvecs=int(nr.matvecs[i]), tmatvecs=int(nr.tmatvecs[i]), dots=int(nr.dots[i]),
+            sketches=int(nr.sketches[i]), wall_ms=float(nr.wall[i]), rank_fallback=bool(nr.rankfb[i]),
+        ))
+    fact = DeviceFactorization(nr, square, A.rows, A.cols)
+    return SolveResult(x=nr.x, trace=trace, termination=term, factorization=fact, loop_ms=nr.loop_ms)
+
+
+def scmrh(A, b, cfg=None, x_true=None, *, sketch_basis=False, sketch=None):
+    """Sketched projected minimal residual on the square Hessenberg basis
+    (solvers.py:562-574)."""
+    return _hessenberg_solve(A, b, cfg, x_true, True, sketch_basis, sketch)
+
+
+def slslu(A, b, cfg=None, x_true=None, *, sketch_basis=False, sketch=None):
+    """Sketched projected least squares on the generalized bases (solvers.py:577-581)."""
+    return _hessenberg_solve(A, b, cfg, x_true, False, sketch_basis, sketch)
+
+
+def scmrh_tikhonov(A, b, cfg=None, x_true=None):
+    """scmrh with the sketched penalty lam^2 |S1 L_k y|^2 (solvers.py:584-591)."""
+    return _hessenberg_solve(A, b, cfg, x_true, True, False)
+
+
+def slslu_tikhonov(A, b, cfg=None, x_true=None, *, printed_f_columns=False):
+    """slslu with the sketched penalty (solvers.py:594-605)."""
+    if printed_f_columns:
+        raise NotImplementedError("the printed-F comparison variant is out of scope")
+    return _hessenberg_solve(A, b, cfg, x_true, False, False)
+
+
+SOLVERS = {
+    "scmrh": scmrh,
+    "slslu": slslu,
+}

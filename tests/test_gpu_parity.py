@@ -1,0 +1,413 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle and the
+reference's golden fixtures.  Bit-exact for operator row sums, pivots, bases
+and H/W; tolerances stated per test for the projected-solve quantities."""
+
+import numpy as np
+import pytest
+import scipy.sparse
+
+pytestmark = pytest.mark.gpu
+
+from oracle import hessketch_oracle as ho  # noqa: E402
+from oracle import tomo_oracle as to  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def hs():
+    import paper_2502_02721_b200 as hs
+    from paper_2502_02721_b200 import _lib
+
+    _lib.load()  # fail loudly if the extension is missing
+    return hs
+
+
+def _csr(g, prefix="A_"):
+    shape = tuple(int(s) for s in g[prefix + "shape"])
+    return scipy.sparse.csr_matrix((g[prefix + "data"], g[prefix + "indices"], g[prefix + "indptr"]), shape=shape)
+
+
+def _rel(a, b):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+# ---------------------------------------------------------------------------
+# operators
+
+
+def test_csr_operator_bitwise(hs, golden):
+    g = golden("tomo_matrices")
+    M = _csr(g, "tomo16x12_")
+    rng = np.random.default_rng(1)
+    op = hs.CsrOperator(M)
+    x = rng.standard_normal(M.shape[1])
+    y = rng.standard_normal(M.shape[0])
+    np.testing.assert_array_equal(op.matvec(x), M @ x)
+    np.testing.assert_array_equal(op.rmatvec(y), M.T.tocsr() @ y)
+    # fp32 values / fp32 work == scipy float32 csr_matvec
+    M32 = M.astype(np.float32)
+    op32 = hs.CsrOperator(M32)
+    x32 = x.astype(np.float32)
+    np.testing.assert_array_equal(op32.matvec(x32, np.float32), M32 @ x32)
+    np.testing.assert_array_equal(op32.rmatvec(y.astype(np.float32), np.float32), M32.T.tocsr() @ y.astype(np.float32))
+    # fp32 values, fp64 work: exact upcast as scipy does for float32 @ float64
+    np.testing.assert_array_equal(op32.matvec(x), M32 @ x)
+
+
+def test_csr_random_long_rows_and_empty_rows(hs):
+    rng = np.random.default_rng(2)
+    M = scipy.sparse.random(300, 5000, density=0.2, random_state=3, format="csr")
+    M = M.tolil()
+    M[5, :] = 0
+    M[77, :] = 0
+    M = M.tocsr()
+    op = hs.CsrOperator(M)
+    x = rng.standard_normal(5000)
+    got = op.matvec(x)
+    np.testing.assert_array_equal(got, M @ x)
+    assert got[5] == 0.0 and got[77] == 0.0
+    y = rng.standard_normal(300)
+    np.testing.assert_array_equal(op.rmatvec(y), M.T.tocsr() @ y)
+    At = op.export(transpose=True)
+    ref = M.T.tocsr()
+    np.testing.assert_array_equal(At.indptr, ref.indptr)
+    np.testing.assert_array_equal(At.indices, ref.indices)
+    np.testing.assert_array_equal(At.data, ref.data)
+
+
+def test_dense_operator_bitwise_sequential(hs):
+    rng = np.random.default_rng(4)
+    M = rng.standard_normal((70, 45))
+    op = hs.DenseOperator(M)
+    x = rng.standard_normal(45)
+    y = rng.standard_normal(70)
+    np.testing.assert_array_equal(op.matvec(x), ho.sequential_rows(M, x))
+    np.testing.assert_array_equal(op.rmatvec(y), ho.sequential_rows(np.ascontiguousarray(M.T), y))
+    M32 = M.astype(np.float32)
+    op32 = hs.DenseOperator(M32)
+    np.testing.assert_array_equal(op32.matvec(x.astype(np.float32), np.float32), ho.sequential_rows(M32, x.astype(np.float32)))
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("shape,ks", [((16, 16), (5, 5)), ((33, 70), (3, 7)), ((64, 64), (15, 15))])
+def test_psf_stencil_bitwise(hs, dt, shape, ks):
+    rng = np.random.default_rng(5)
+    K = rng.random(ks)
+    K /= K.sum()
+    op = hs.PsfOperator(shape, K, dtype=dt)
+    img = rng.standard_normal(shape).astype(dt)
+    np.testing.assert_array_equal(op.matvec(img.ravel(), dt), to.psf_stencil(img, K, False, dt).ravel())
+    np.testing.assert_array_equal(op.rmatvec(img.ravel(), dt), to.psf_stencil(img, K, True, dt).ravel())
+
+
+def test_tomography_builder_matches_reference(hs, golden):
+    g = golden("tomo_matrices")
+    for grid, angles in ((8, 6), (13, 7), (16, 12)):
+        want = _csr(g, f"tomo{grid}x{angles}_")
+        op = hs.TomographyOperator(grid, angles, dtype=np.float64)
+        got = op.export()
+        np.testing.assert_array_equal(got.indptr, want.indptr)
+        np.testing.assert_array_equal(got.indices, want.indices)
+        np.testing.assert_array_equal(got.data, want.data)
+        gt = op.export(transpose=True)
+        wt = want.T.tocsr()
+        np.testing.assert_array_equal(gt.indptr, wt.indptr)
+        np.testing.assert_array_equal(gt.indices, wt.indices)
+        np.testing.assert_array_equal(gt.data, wt.data)
+
+
+@pytest.mark.parametrize("grid,angles,bins", [(32, 20, 45), (40, 17, 31), (64, 36, 91)])
+def test_tomography_builder_general_bins(hs, grid, angles, bins):
+    want = to.tomography_matrix(grid, angles, bins)
+    op = hs.TomographyOperator(grid, angles, bins, dtype=np.float64)
+    got = op.export()
+    np.testing.assert_array_equal(got.indptr, want.indptr)
+    np.testing.assert_array_equal(got.indices, want.indices)
+    np.testing.assert_array_equal(got.data, want.data)
+    op32 = hs.TomographyOperator(grid, angles, bins, dtype=np.float32)
+    np.testing.assert_array_equal(op32.export().data, want.data.astype(np.float32).astype(np.float64))
+
+
+# ---------------------------------------------------------------------------
+# sketches
+
+
+def test_sketches(hs):
+    rng = np.random.default_rng(6)
+    v = rng.standard_normal(3000)
+    S = rng.standard_normal((50, 3000))
+    dense = hs.device_sketch(hs.SketchOperator(50, 3000, 0, S))
+    np.testing.assert_allclose(dense.apply(v), S @ v, rtol=1e-12, atol=1e-12)
+    gs = hs.GaussianSketch(64, 3000, seed=9)
+    Sg = gs.materialize()
+    np.testing.assert_allclose(gs.apply(v), Sg @ v, rtol=1e-10, atol=1e-10)
+    assert abs(Sg.var() * 64 - 1.0) < 0.02 and abs(Sg.mean()) < 0.01
+    ss = hs.SparseSignSketch(40, 3000, seed=3, zeta=8)
+    Ss = ss.materialize()
+    assert Ss.nnz == 3000 * 8
+    col_counts = np.diff(Ss.tocsc().indptr)
+    assert np.all(col_counts == 8)
+    np.testing.assert_allclose(np.abs(Ss.data), 1 / np.sqrt(8))
+    np.testing.assert_allclose(ss.apply(v), Ss @ v, rtol=1e-12, atol=1e-12)
+    csr = hs.device_sketch(hs.SketchOperator(40, 3000, 0, Ss))
+    np.testing.assert_allclose(csr.apply(v), Ss @ v, rtol=1e-12, atol=1e-12)
+    # determinism
+    np.testing.assert_array_equal(hs.GaussianSketch(64, 3000, seed=9).materialize(), Sg)
+
+
+# ---------------------------------------------------------------------------
+# solver parity against the reference fixtures (fp64)
+
+
+def _check(res, g, prefix="", bitwise_basis=True, rtol=1e-10):
+    assert res.termination == str(g[prefix + "termination"])
+    recs = res.trace.records
+    assert len(recs) == len(g[prefix + "sres_norm"])
+    for name in ("matvecs", "tmatvecs", "dots", "sketches"):
+        assert [getattr(r, name) for r in recs] == list(g[prefix + name]), name
+    st = res.factorization
+    np.testing.assert_array_equal(st.t[: len(g[prefix + "t"])], g[prefix + "t"])
+    if prefix + "g" in g:
+        np.testing.assert_array_equal(st.g[: len(g[prefix + "g"])], g[prefix + "g"])
+    if bitwise_basis:
+        np.testing.assert_array_equal(st.H_matrix(), g[prefix + "H"])
+        np.testing.assert_array_equal(st.L_matrix(), g[prefix + "L"])
+        if prefix + "W" in g:
+            np.testing.assert_array_equal(st.W_matrix(), g[prefix + "W"])
+            np.testing.assert_array_equal(st.D_matrix(), g[prefix + "D"])
+    else:
+        np.testing.assert_allclose(st.H_matrix(), g[prefix + "H"], rtol=1e-9, atol=1e-12)
+    sres = np.array([r.sres_norm for r in recs])
+    proj = np.array([r.proj_obj for r in recs])
+    # north_star: 1e-10 relative in fp64 (early iterations)
+    np.testing.assert_allclose(sres, g[prefix + "sres_norm"], rtol=rtol)
+    np.testing.assert_allclose(proj, g[prefix + "proj_obj"], rtol=rtol)
+    assert _rel(res.x, g[prefix + "x"]) <= rtol
+    if not np.all(np.isnan(g[prefix + "rel_err"])):
+        np.testing.assert_allclose([r.rel_err for r in recs], g[prefix + "rel_err"], rtol=rtol)
+
+
+def test_scmrh_dense_vs_reference(hs, golden):
+    g = golden("scmrh_dense")
+    A = hs.LinearOperator.from_matrix(g["M"])
+    res = hs.scmrh(A, g["b"], hs.SolverConfig(maxiter=12, seed=5), x_true=g["x_true"])
+    _check(res, g, bitwise_basis=False, rtol=1e-9)
+    res = hs.scmrh(A, g["b"], hs.SolverConfig(maxiter=8), x_true=g["x_true"],
+                   sketch=hs.SketchOperator(40, 40, 0, g["S2_orth"]))
+    _check(res, g, "orth_", bitwise_basis=False, rtol=1e-9)
+    res = hs.scmrh(A, g["b"], hs.SolverConfig(maxiter=6, seed=2, x0=g["x0"]))
+    _check(res, g, "x0_", bitwise_basis=False, rtol=1e-9)
+    res = hs.scmrh_tikhonov(A, g["b"], hs.SolverConfig(maxiter=7, seed=3, lam=0.4))
+    _check(res, g, "tik_", bitwise_basis=False, rtol=1e-9)
+
+
+def test_slslu_dense_vs_reference(hs, golden):
+    g = golden("slslu_dense")
+    A = hs.LinearOperator.from_matrix(g["M"])
+    res = hs.slslu(A, g["b"], hs.SolverConfig(maxiter=10, seed=7), x_true=g["x_true"])
+    _check(res, g, bitwise_basis=False, rtol=1e-9)
+    res = hs.slslu_tikhonov(A, g["b"], hs.SolverConfig(maxiter=9, seed=3, lam=0.7), x_true=g["x_true"])
+    _check(res, g, "tik_", bitwise_basis=False, rtol=1e-9)
+    res = hs.slslu(hs.LinearOperator.from_matrix(g["Mw"]), g["bw"], hs.SolverConfig(maxiter=9, seed=1))
+    _check(res, g, "w_", bitwise_basis=False, rtol=1e-9)
+    res = hs.slslu(hs.LinearOperator.from_matrix(g["Mh"]), np.array([1.0, 3.0]), hs.SolverConfig(maxiter=1, seed=0))
+    _check(res, g, "h_", bitwise_basis=False, rtol=1e-9)
+
+
+def test_slslu_tomography_vs_reference_bitwise(hs, golden):
+    """CSR operator: basis, pivots, H and W bit-identical to the reference."""
+    g = golden("slslu_tomo16")
+    K = _csr(g)
+    S2 = _csr(g, "S2_")
+    A = hs.LinearOperator.from_matrix(K)
+    sk = hs.SketchOperator(S2.shape[0], S2.shape[1], 9, S2)
+    res = hs.slslu(A, g["b"], hs.SolverConfig(maxiter=40), x_true=g["x_true"], sketch=sk)
+    _check(res, g, rtol=1e-10)
+    res = hs.slslu(A, g["b"], hs.SolverConfig(maxiter=30, lam=1e-3, seed=11), x_true=g["x_true"], sketch=sk)
+    _check(res, g, "tik_", rtol=1e-10)
+
+
+def test_reference_from_matrix_operator_is_accepted(hs, golden):
+    """A reference-style LinearOperator built by from_matrix (closure over a
+    scipy matrix) is recognised and run on the device."""
+    g = golden("slslu_tomo16")
+    K = _csr(g)
+
+    class RefStyle:
+        def __init__(self, M):
+            Mt = M.T.tocsr()
+            self.rows, self.cols = M.shape
+            self.forward = lambda x: M @ x
+            self.transpose = lambda y: Mt @ y
+
+        @property
+        def is_square(self):
+            return self.rows == self.cols
+
+    S2 = _csr(g, "S2_")
+    res = hs.slslu(RefStyle(K), g["b"], hs.SolverConfig(maxiter=40), x_true=g["x_true"],
+                   sketch=hs.SketchOperator(60, K.shape[0], 9, S2))
+    _check(res, g, rtol=1e-10)
+
+
+def test_python_callables_rejected(hs):
+    A = hs.LinearOperator(4, 4, lambda x: x, lambda y: y)
+    with pytest.raises(TypeError):
+        hs.scmrh(A, np.ones(4), hs.SolverConfig(maxiter=2))
+
+
+def test_edge_cases_vs_reference(hs, golden):
+    g = golden("edge_cases")
+    res = hs.scmrh(hs.LinearOperator.identity(5), g["id_b"], hs.SolverConfig(maxiter=3, seed=42))
+    _check(res, g, "id_", bitwise_basis=False)
+    np.testing.assert_allclose(res.x, g["id_b"], atol=1e-12)
+    res = hs.slslu(hs.LinearOperator.from_matrix(np.ones((4, 3))), np.zeros(4), hs.SolverConfig(maxiter=2))
+    assert res.termination == "trivial" and np.array_equal(res.x, np.zeros(3))
+    res = hs.slslu(hs.LinearOperator.from_matrix(np.array([[1.0], [0.0]])), np.array([0.0, 1.0]),
+                   hs.SolverConfig(maxiter=2))
+    assert res.termination == "trivial"
+    res = hs.scmrh(hs.LinearOperator.from_matrix(g["tie_M"]), g["tie_b"], hs.SolverConfig(maxiter=3, seed=1))
+    _check(res, g, "tie_", bitwise_basis=False)
+
+
+def test_validation_errors(hs):
+    A = hs.LinearOperator.from_matrix(np.eye(8) * 2.0 + 0.1)
+    with pytest.raises(ValueError):
+        hs.scmrh(A, np.ones(8), hs.SolverConfig(maxiter=6, sketch_rows=4))
+    with pytest.raises(ValueError):
+        hs.scmrh(hs.LinearOperator.from_matrix(np.ones((3, 2))), np.ones(3), hs.SolverConfig(maxiter=2))
+    with pytest.raises(ValueError):
+        hs.slslu(A, np.ones(7), hs.SolverConfig(maxiter=2))
+    with pytest.raises(NotImplementedError):
+        hs.scmrh(A, np.ones(8), hs.SolverConfig(maxiter=2, compute_diagnostics=True))
+
+
+def test_deterministic_replay(hs):
+    rng = np.random.default_rng(20)
+    M = rng.standard_normal((16, 16)) + 4 * np.eye(16)
+    A = hs.LinearOperator.from_matrix(M)
+    b = rng.standard_normal(16)
+    cfg = hs.SolverConfig(maxiter=6, seed=11)
+    r1 = hs.scmrh(A, b, cfg)
+    r2 = hs.scmrh(A, b, cfg)
+    assert np.array_equal(r1.x, r2.x)
+    assert r1.trace.column("sres_norm") == r2.trace.column("sres_norm")
+    assert r1.trace.column("proj_obj") == r2.trace.column("proj_obj")
+
+
+def test_sketch_basis_matches_column_sketching(hs):
+    rng = np.random.default_rng(22)
+    M = rng.standard_normal((14, 14)) + 4 * np.eye(14)
+    A = hs.LinearOperator.from_matrix(M)
+    b = rng.standard_normal(14)
+    cfg = hs.SolverConfig(maxiter=6, seed=5)
+    direct = hs.scmrh(A, b, cfg)
+    via = hs.scmrh(A, b, cfg, sketch_basis=True)
+    np.testing.assert_allclose(direct.x, via.x, rtol=1e-7, atol=1e-10)
+    assert via.trace.final().sketches == 1 + 1 + 6
+
+
+# ---------------------------------------------------------------------------
+# fp32 device path against oracle32, at sizes the oracle finishes in seconds
+
+
+def _oracle_tomo(grid, angles, bins, dt, maxiter, lam, S2, seed=0):
+    from paper_2502_02721_b200.problems import add_noise, random_ellipses
+
+    K = to.tomography_matrix(grid, angles, bins)
+    x = random_ellipses(grid, 10, seed).ravel()
+    b, _ = add_noise(K @ x, 0.01, seed + 1)
+    A = ho.csr_operator(K, dt)
+    S1 = None
+    if lam > 0:
+        S1 = ho.gaussian_sketch_entries(S2.shape[0], K.shape[1], ho.derive_seed(seed, 1))
+    res = ho.hessenberg_solve(A, b, square=False, maxiter=maxiter, S2=S2, S1=S1, lam=lam, x_true=x)
+    return K, b, x, res
+
+
+@pytest.mark.parametrize("lam", [0.0, 1e-3])
+def test_fp32_tomography_vs_oracle32(hs, lam):
+    grid, angles, bins, maxiter = 48, 30, 69, 40
+    ss = hs.SparseSignSketch(200, angles * bins, seed=5, zeta=8)
+    S2 = ss.materialize()
+    K, b, x, ref = _oracle_tomo(grid, angles, bins, np.float32, maxiter, lam, S2)
+    op = hs.TomographyOperator(grid, angles, bins, dtype=np.float32)
+    cfg = hs.SolverConfig(maxiter=maxiter, lam=lam, seed=0, dtype="float32", sketch_kind="pcg64")
+    res = hs.slslu(op, b, cfg, x_true=x, sketch=hs.SketchOperator(200, op.rows, 5, ss))
+    st = res.factorization
+    t_ref, g_ref = ho.pivots_of(ref.state)
+    np.testing.assert_array_equal(st.t[: len(t_ref)], t_ref)
+    np.testing.assert_array_equal(st.g[: len(g_ref)], g_ref)
+    np.testing.assert_array_equal(st.H_matrix(), ref.state.H_matrix())
+    np.testing.assert_array_equal(st.W_matrix(), ref.state.W_matrix())
+    np.testing.assert_array_equal(st.L_matrix(), np.column_stack(ref.state.L).astype(np.float64))
+    np.testing.assert_array_equal(st.D_matrix(), np.column_stack(ref.state.D).astype(np.float64))
+    # north_star: 1e-4 relative in fp32
+    np.testing.assert_allclose(res.trace.column("sres_norm"), ref.column("sres_norm"), rtol=1e-4)
+    np.testing.assert_allclose(res.trace.column("rel_err"), ref.column("rel_err"), rtol=1e-4)
+    assert _rel(res.x, ref.x) <= 1e-4
+
+
+def test_fp32_deblur_vs_oracle32(hs):
+    from paper_2502_02721_b200.problems import add_noise, gaussian_psf, rectangles_and_discs
+
+    size, maxiter = 48, 40
+    psf = gaussian_psf(2.0, radius=7)
+    x = rectangles_and_discs(size, 20, 0).ravel()
+    op = hs.PsfOperator(size, psf, dtype=np.float32)
+    b, _ = add_noise(op.matvec(x), 0.01, 1)
+    gs = hs.GaussianSketch(160, size * size, seed=3)
+    S = gs.materialize()
+    A = ho.Operator(size * size, size * size,
+                    lambda v: to.psf_stencil(v.reshape(size, size), psf, False, np.float32).ravel(),
+                    lambda v: to.psf_stencil(v.reshape(size, size), psf, True, np.float32).ravel(), np.float32)
+    ref = ho.hessenberg_solve(A, b, square=True, maxiter=maxiter, S2=S, x_true=x)
+    res = hs.scmrh(op, b, hs.SolverConfig(maxiter=maxiter, dtype="float32"), x_true=x,
+                   sketch=hs.SketchOperator(160, size * size, 3, gs))
+    t_ref, _ = ho.pivots_of(ref.state)
+    np.testing.assert_array_equal(res.factorization.t[: len(t_ref)], t_ref)
+    np.testing.assert_array_equal(res.factorization.H_matrix(), ref.state.H_matrix())
+    np.testing.assert_allclose(res.trace.column("sres_norm"), ref.column("sres_norm"), rtol=1e-4)
+    assert _rel(res.x, ref.x) <= 1e-4
+
+
+def test_bf16_basis_keeps_structure(hs):
+    """bf16 storage: pivots exact 1.0, exact zeros at earlier pivots."""
+    from paper_2502_02721_b200.problems import add_noise, gaussian_psf, piecewise_constant
+
+    size = 64
+    psf = gaussian_psf(4.0, radius=15)
+    op = hs.PsfOperator(size, psf, dtype=np.float32)
+    x = piecewise_constant(size, 0).ravel()
+    b, _ = add_noise(op.matvec(x), 0.005, 1)
+    cfg = hs.SolverConfig(maxiter=20, dtype="float32", basis_dtype="bfloat16", sketch_kind="gaussian", sketch_rows=120)
+    res = hs.scmrh(op, b, cfg, x_true=x)
+    st = res.factorization
+    L = st.L_matrix()
+    t = st.t[: L.shape[1]]
+    B = L[t, :]
+    assert np.all(np.diag(B) == 1.0)
+    assert np.all(np.triu(B, 1) == 0.0)
+    ref = hs.scmrh(op, b, hs.SolverConfig(maxiter=20, dtype="float32", sketch_kind="gaussian", sketch_rows=120), x_true=x)
+    assert abs(res.trace.final().rel_err - ref.trace.final().rel_err) < 0.05
+
+
+def test_relations_at_scale(hs):
+    """Size-independent properties on a 256^2 tomography sLSLU run:
+    unit-triangular bases at the pivots (exact) and A L_k = D_{k+1} H."""
+    from paper_2502_02721_b200.problems import make_workload
+
+    w = make_workload(3, scale=128, maxiter=25)
+    res = hs.slslu(w.operator, w.b, w.cfg, x_true=w.x_true, sketch=w.sketch)
+    st = res.factorization
+    D, L = st.D_matrix(), st.L_matrix()
+    Dt = D[st.t[: D.shape[1]], :]
+    Lt = L[st.g[: L.shape[1]], :]
+    assert np.all(np.diag(Dt) == 1.0) and np.all(np.triu(Dt, 1) == 0.0)
+    assert np.all(np.diag(Lt) == 1.0) and np.all(np.triu(Lt, 1) == 0.0)
+    K = w.operator.export().astype(np.float64)
+    k = st.k
+    H = st.H_matrix(rows=D.shape[1])
+    lhs = K @ L[:, :k]
+    assert np.linalg.norm(lhs - D @ H) <= 1e-4 * np.linalg.norm(lhs)
+    assert all(r.dots == 0 for r in res.trace.records)
