@@ -206,6 +206,41 @@ struct Csr {
   DBuf rowptr, col, val;
 };
 
+// SELL-32x4 copy of a CSR (hs_ops.cuh: sell_spmv_kernel)
+struct Sell {
+  long long rows = 0, cols = 0, nnz = 0, slots = 0, nslices = 0;
+  DBuf sptr, rlen, col, val;
+  bool ready() const { return nslices > 0 || rows == 0 ? sptr.p != nullptr : false; }
+};
+
+template <class V>
+static void csr_to_sell(hs_ctx* ctx, const Csr& A, Sell& S) {
+  cudaStream_t s = ctx->stream;
+  S.rows = A.rows;
+  S.cols = A.cols;
+  S.nnz = A.nnz;
+  S.nslices = (A.rows + 31) / 32;
+  S.rlen.alloc(std::max<long long>(A.rows, 1) * sizeof(int), false);
+  DBuf slots((S.nslices + 1) * sizeof(long long));
+  sell_slice_chunks_kernel<<<grid_for(S.nslices, 8, 1 << 30), 256, 0, s>>>(
+      A.rows, S.nslices, A.rowptr.as<long long>(), S.rlen.as<int>(), slots.as<long long>());
+  CKL();
+  S.sptr.alloc((S.nslices + 1) * sizeof(long long), false);
+  size_t tmp = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, slots.as<long long>(), S.sptr.as<long long>(), S.nslices + 1, s));
+  DBuf t(tmp, false);
+  CK(cub::DeviceScan::ExclusiveSum(t.p, tmp, slots.as<long long>(), S.sptr.as<long long>(), S.nslices + 1, s));
+  CK(cudaMemcpyAsync(&S.slots, S.sptr.as<long long>() + S.nslices, sizeof(long long), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  S.col.alloc(std::max<long long>(S.slots, 4) * sizeof(int), false);
+  S.val.alloc(std::max<long long>(S.slots, 4) * sizeof(V), false);
+  sell_fill_kernel<V><<<grid_for(S.nslices, 8, 1 << 30), 256, 0, s>>>(
+      A.rows, S.nslices, A.rowptr.as<long long>(), A.col.as<int>(), A.val.as<V>(), S.sptr.as<long long>(),
+      S.col.as<int>(), S.val.as<V>());
+  CKL();
+  CK(cudaStreamSynchronize(s));
+}
+
 struct hs_op {
   hs_ctx* ctx = nullptr;
   int kind = OP_DENSE;
@@ -213,8 +248,14 @@ struct hs_op {
   long long m = 0, n = 0;
   // dense: column-major A (m x n) and column-major A^T (n x m)
   DBuf Acm, Atcm;
-  // csr
+  // csr (kept for export / small operators) and the SELL-32x4 copies used by the loop
   Csr A, At;
+  Sell As, Ats;
+  bool csr_kept = true;
+  // tomography: per-slice transposed-layout flags of As and the scratch copy of x
+  int img_grid = 0;
+  DBuf sflag;
+  mutable DBuf xT;
   // psf
   int H = 0, W = 0, kh = 0, kw = 0;
   DBuf K;
@@ -224,7 +265,28 @@ struct hs_op {
     cudaStream_t s = ctx->stream;
     const Tin* xi = reinterpret_cast<const Tin*>(x);
     T* yo = reinterpret_cast<T*>(y);
-    if (kind == OP_CSR) {
+    if (kind == OP_CSR && (transpose ? Ats.nslices : As.nslices) > 0) {
+      const Sell& M = transpose ? Ats : As;
+      const int grid = grid_for(M.nslices, 8, ctx->num_sms * 16);
+      const double bytes = (double)M.nnz * (sizeof(V) + 4) + (double)M.rows * 4 + (double)M.nslices * 8 +
+                           (double)M.cols * sizeof(Tin) + (double)M.rows * sizeof(T);
+      const bool tflag = !transpose && sflag.p != nullptr;
+      if (tflag) {
+        // transposed image copy of x for the near-horizontal ray slices
+        Prof p(ctx, "x_transpose", 2.0 * (double)n * sizeof(Tin));
+        const size_t need = (size_t)n * sizeof(Tin);
+        if (xT.bytes < need) xT.alloc(need, false);
+        dim3 tg((img_grid + 31) / 32, (img_grid + 31) / 32);
+        image_transpose_kernel<Tin><<<tg, 256, 0, s>>>(img_grid, xi, xT.as<Tin>());
+        CKL();
+      }
+      Prof p(ctx, transpose ? "spmv_AT" : "spmv_A", bytes);
+      sell_spmv_kernel<V, Tin, T><<<grid, 256, 0, s>>>(M.rows, M.nslices, M.sptr.as<long long>(), M.rlen.as<int>(),
+                                                      M.col.as<int>(), M.val.as<V>(), xi,
+                                                      tflag ? xT.as<Tin>() : nullptr,
+                                                      tflag ? sflag.as<unsigned char>() : nullptr, yo);
+      CKL();
+    } else if (kind == OP_CSR) {
       const Csr& M = transpose ? At : A;
       constexpr int WARPS = sizeof(T) == 8 ? 4 : 8, CH = 32;
       const long long tiles = (M.rows + 31) / 32;

@@ -155,3 +155,211 @@ psf_stencil_kernel(int H, int W, int kh, int kw, const V* __restrict__ K,
 }
 
 }  // namespace hs
+
+namespace hs {
+
+// --------------------------------------------------------------------------
+// SELL-32x4: the device layout of the tomography operators.
+//
+// Rows are grouped in slices of 32 consecutive rows (adjacent parallel rays
+// for A, adjacent pixels for A^T).  Inside a slice, entry e of the slice's
+// row r sits at slot  sptr[s] + (e/4)*128 + r*4 + e%4:  chunk q of a slice
+// is 512 contiguous bytes of values (fp32) holding entries 4q..4q+3 of each
+// of the 32 rows.  A warp owns a slice, lane r owns row r: every load of the
+// (value, column) stream is one fully coalesced 128-bit access per lane, and
+// each lane still adds ITS OWN row's products strictly left to right
+// (product rounded, then added; scipy csr_matvec order).  Rows shorter than
+// the slice's longest row are padded to it (zeros, never added).
+//
+// The x gathers of the 32 lanes hit the same few sectors at every step
+// (adjacent rays at the same depth), and a lane's next gather usually falls
+// in the sector its previous one loaded, so x is served from L1; the matrix
+// stream is loaded with the evict-first (.cs) policy to keep x resident in L2.
+
+template <class V> struct Chunk4;
+template <> struct Chunk4<float> {
+  float v[4];
+  static __device__ __forceinline__ Chunk4 load(const float* p) {
+    float4 t = __ldcs(reinterpret_cast<const float4*>(p));
+    return Chunk4{{t.x, t.y, t.z, t.w}};
+  }
+};
+template <> struct Chunk4<double> {
+  double v[4];
+  static __device__ __forceinline__ Chunk4 load(const double* p) {
+    double2 a = __ldcs(reinterpret_cast<const double2*>(p));
+    double2 b = __ldcs(reinterpret_cast<const double2*>(p) + 1);
+    return Chunk4{{a.x, a.y, b.x, b.y}};
+  }
+};
+
+template <class T, class Tin> __device__ __forceinline__ T gather_x(const Tin* __restrict__ x, int c) {
+  return cvt<T>(__ldg(x + c));
+}
+template <> __device__ __forceinline__ float gather_x<float, __nv_bfloat16>(const __nv_bfloat16* __restrict__ x, int c) {
+  return __bfloat162float(x[c]);
+}
+
+// xT / sflag (optional): slices whose flag is set store their column indices
+// in the TRANSPOSED image layout and gather from xT (the image transposed).
+// Used for near-horizontal rays of the tomography operator, whose 32 lanes
+// step through 32 adjacent image rows: in the transposed layout those are 32
+// adjacent words (one 128-byte line) instead of 32 lines.  Entry order, and
+// with it the summation order, is unchanged.
+template <class V, class Tin, class T>
+__global__ void __launch_bounds__(256)
+sell_spmv_kernel(long long rows, long long nslices, const long long* __restrict__ sptr,
+                 const int* __restrict__ rlen, const int* __restrict__ col, const V* __restrict__ val,
+                 const Tin* __restrict__ xrow, const Tin* __restrict__ xT, const unsigned char* __restrict__ sflag,
+                 T* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const long long wstride = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long s = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); s < nslices; s += wstride) {
+    const Tin* __restrict__ x = (sflag != nullptr && sflag[s]) ? xT : xrow;
+    const long long row = s * 32 + lane;
+    const int len = row < rows ? rlen[row] : 0;
+    const long long base = sptr[s];
+    const int nq_slice = (int)((sptr[s + 1] - base) >> 7);
+    const int nq = (len + 3) >> 2;
+    const int* cp = col + base + lane * 4;
+    const V* vp = val + base + lane * 4;
+    T acc = T(0);
+    if (nq > 0) {
+      // software pipeline: chunk q+1's (column, value) loads are in flight
+      // while chunk q's gathers and adds run
+      int4 c = __ldcs(reinterpret_cast<const int4*>(cp));
+      Chunk4<V> v = Chunk4<V>::load(vp);
+      for (int q = 0; q < nq; ++q) {
+        int4 cn = c;
+        Chunk4<V> vn = v;
+        if (q + 1 < nq) {
+          cn = __ldcs(reinterpret_cast<const int4*>(cp + (long long)(q + 1) * 128));
+          vn = Chunk4<V>::load(vp + (long long)(q + 1) * 128);
+        }
+        const int e = q * 4;
+        const T x0 = gather_x<T>(x, c.x);
+        const T x1 = (e + 1 < len) ? gather_x<T>(x, c.y) : T(0);
+        const T x2 = (e + 2 < len) ? gather_x<T>(x, c.z) : T(0);
+        const T x3 = (e + 3 < len) ? gather_x<T>(x, c.w) : T(0);
+        acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[0]), x0));
+        if (e + 1 < len) acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[1]), x1));
+        if (e + 2 < len) acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[2]), x2));
+        if (e + 3 < len) acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[3]), x3));
+        c = cn;
+        v = vn;
+      }
+    }
+    (void)nq_slice;
+    if (row < rows) y[row] = acc;
+  }
+}
+
+// ---- image transpose (grid x grid), 32x32 smem tiles --------------------------------
+template <class Tin>
+__global__ void __launch_bounds__(256) image_transpose_kernel(int grid, const Tin* __restrict__ x, Tin* __restrict__ xT) {
+  __shared__ Tin tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows of threads
+  for (int r = ty; r < 32; r += 8) {
+    const int gy = by + r, gx = bx + tx;
+    if (gy < grid && gx < grid) tile[r][tx] = x[(long long)gy * grid + gx];
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int gx = bx + r, gy = by + tx;  // output row = original column
+    if (gx < grid && gy < grid) xT[(long long)gx * grid + gy] = tile[tx][r];
+  }
+}
+
+// Choose, per slice, the image layout in which the 32 lanes' gathers touch
+// the fewest 128-byte lines (sampled at 8 depths), and remap the slice's
+// column indices r*grid + c -> c*grid + r when the transposed layout wins.
+// (Adjacent rays entering through the left/right edge differ in y at equal
+// depth -> transposed; through the bottom edge they differ in x -> row-major.)
+__global__ void sell_transpose_cols_kernel(long long nslices, long long rows, int n_bins, int grid,
+                                           const double* __restrict__ cos_t, const double* __restrict__ sin_t,
+                                           const long long* __restrict__ sptr, const int* __restrict__ rlen,
+                                           int* __restrict__ col, unsigned char* __restrict__ sflag) {
+  const long long s = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (s >= nslices) return;
+  (void)n_bins;
+  (void)cos_t;
+  (void)sin_t;
+  const int lane = threadIdx.x & 31;
+  const long long row = s * 32 + lane;
+  const int len = row < rows ? rlen[row] : 0;
+  const long long base = sptr[s];
+  const int slots = (int)((sptr[s + 1] - base) >> 5);  // entries per row incl. padding
+  int lines_row = 0, lines_t = 0;
+  for (int k = 0; k < 8; ++k) {
+    const int e = (int)(((long long)slots * (2 * k + 1)) / 16);
+    const bool has = e < len;
+    const unsigned act = __ballot_sync(0xffffffffu, has);
+    if (act == 0) continue;
+    int c = 0;
+    if (has) c = col[base + (long long)(e >> 2) * 128 + lane * 4 + (e & 3)];
+    const int lr = has ? (c >> 5) : -1 - lane;
+    const int lt = has ? (((c % grid) * grid + (c / grid)) >> 5) : -1 - lane;
+    const unsigned mr = __match_any_sync(0xffffffffu, lr);
+    const unsigned mt = __match_any_sync(0xffffffffu, lt);
+    // leaders (lowest lane of each group) count distinct lines
+    lines_row += __popc(__ballot_sync(0xffffffffu, has && (__ffs(mr) - 1) == lane));
+    lines_t += __popc(__ballot_sync(0xffffffffu, has && (__ffs(mt) - 1) == lane));
+  }
+  const bool use_t = lines_t < lines_row;
+  if (lane == 0) sflag[s] = use_t ? 1 : 0;
+  if (!use_t) return;
+  for (long long p = sptr[s] + lane; p < sptr[s + 1]; p += 32) {
+    const int c = col[p];
+    col[p] = (c % grid) * grid + (c / grid);
+  }
+}
+
+// ---- CSR -> SELL-32x4 conversion ------------------------------------------------
+// per slice: number of 4-entry chunks of its longest row
+__global__ void sell_slice_chunks_kernel(long long rows, long long nslices, const long long* __restrict__ rowptr,
+                                         int* __restrict__ rlen, long long* __restrict__ slice_slots) {
+  const long long s = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (s >= nslices) return;
+  const int lane = threadIdx.x & 31;
+  const long long row = s * 32 + lane;
+  int len = 0;
+  if (row < rows) {
+    len = (int)(rowptr[row + 1] - rowptr[row]);
+    rlen[row] = len;
+  }
+  int nq = (len + 3) >> 2;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nq = max(nq, __shfl_xor_sync(0xffffffffu, nq, o));
+  if (lane == 0) slice_slots[s] = (long long)nq * 128;
+}
+
+template <class V>
+__global__ void sell_fill_kernel(long long rows, long long nslices, const long long* __restrict__ rowptr,
+                                 const int* __restrict__ ccol, const V* __restrict__ cval,
+                                 const long long* __restrict__ sptr, int* __restrict__ scol, V* __restrict__ sval) {
+  const long long s = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (s >= nslices) return;
+  const int lane = threadIdx.x & 31;
+  const long long row = s * 32 + lane;
+  const long long base = sptr[s];
+  const int nslots = (int)((sptr[s + 1] - base) >> 7) * 4;  // entries per row incl. padding
+  long long r0 = 0;
+  int len = 0;
+  if (row < rows) {
+    r0 = rowptr[row];
+    len = (int)(rowptr[row + 1] - r0);
+  }
+  for (int e = 0; e < nslots; ++e) {
+    const long long slot = base + (long long)(e >> 2) * 128 + lane * 4 + (e & 3);
+    if (e < len) {
+      scol[slot] = ccol[r0 + e];
+      sval[slot] = cval[r0 + e];
+    } else {
+      scol[slot] = 0;
+      sval[slot] = V(0);
+    }
+  }
+}
+
+}  // namespace hs
