@@ -247,14 +247,24 @@ def cpu_baseline(args, w, seconds=None):
 def run_reference(args, ws, rank):
     if rank != 0:
         return None
-    from oracle import cpu_baseline as cb
-    from paper_2502_02721_b200.problems import make_workload
+    from types import SimpleNamespace
 
-    w = make_workload(args.config, seed=args.seed, scale=args.scale, maxiter=args.maxiter)
+    from oracle import cpu_baseline as cb
+
+    if args.config not in (3, 4):
+        return {"impl": "reference", "unavailable": "CPU reference arm implemented for the tomography configs only"}
+    grid, angles, bins, K, ell = (512, 180, 725, 200, 800) if args.config == 3 else (2048, 720, 2897, 300, 1200)
+    if args.scale:
+        f = args.scale / grid
+        grid, angles, bins = args.scale, max(2, round(angles * f)), max(2, round(bins * f))
+    K = args.maxiter or K
+    # host-only workload description (the operator, phantom and b are built on the host by oracle/)
+    w = SimpleNamespace(meta={"grid": grid, "angles": angles, "bins": bins},
+                        cfg=SimpleNamespace(maxiter=K, sketch_rows=max(ell, K + 1)))
     vals = []
     last = None
     for i in range(args.warmup + args.steps):
-        r = cb.run(w, budget_s=args.cpu_seconds)
+        r = cb.run(w, budget_s=args.cpu_seconds / 2)
         if i >= args.warmup:
             vals.append(r["value"])
         last = r

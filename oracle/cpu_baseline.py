@@ -1,0 +1,151 @@
+"""TEST INFRASTRUCTURE ONLY -- CPU baseline for bench.py: the C port of the
+reference's sLSLU loop (oracle/coracle.c) on the host cores, on a bounded
+sample of the benchmark workload.
+
+The host builds its own operator with the C restatement of the reference ray
+tracer (no GPU code on this path), the same seeded phantom and noise, and a
+host-drawn sparse-sign S2 of the same shape and density.  It runs the loop
+until a wall-clock budget is spent, fits the per-iteration time
+t(k) = a + b k over the iterations it completed (k-dependence comes from the
+k-pass elimination and the from-scratch QR), and reports the iteration rate
+extrapolated to the config's full iteration count.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import time
+
+import numpy as np
+import scipy.sparse
+
+from . import build_coracle
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build_coracle.build())
+        vp, i64, i32, dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+        _lib.co_tomo_rowptr.argtypes = [i32, i32, i32, vp, vp, vp, vp, i32]
+        _lib.co_tomo_fill.argtypes = [i32, i32, i32, vp, vp, vp, vp, vp, vp, i32]
+        _lib.co_csr_transpose.argtypes = [i64, i64, vp, vp, vp, vp, vp, vp, i32]
+        _lib.co_slslu_f32.argtypes = [i64, i64, vp, vp, vp, vp, vp, vp, i64, vp, vp, vp, vp, i32, i32, dbl, vp, vp, vp,
+                                      vp, vp]
+        _lib.co_slslu_f32.restype = ctypes.c_int
+        _lib.co_max_threads.restype = ctypes.c_int
+        _lib.co_spmv_f32_f64.argtypes = [i64, vp, vp, vp, vp, vp, i32]
+    return _lib
+
+
+def _p(a):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def host_tomography(grid, n_angles, n_bins, nthreads):
+    """A and A^T (fp32 CSR) built on the host by the C ray tracer."""
+    L = lib()
+    cos_t = np.array([math.cos(math.pi * a / n_angles) for a in range(n_angles)])
+    sin_t = np.array([math.sin(math.pi * a / n_angles) for a in range(n_angles)])
+    offs = np.array([j + 0.5 - n_bins / 2.0 for j in range(n_bins)])
+    m, n = n_angles * n_bins, grid * grid
+    rp = np.zeros(m + 1, dtype=np.int64)
+    L.co_tomo_rowptr(grid, n_angles, n_bins, _p(cos_t), _p(sin_t), _p(offs), _p(rp), nthreads)
+    nnz = int(rp[-1])
+    ci = np.empty(nnz, dtype=np.int32)
+    cv = np.empty(nnz, dtype=np.float32)
+    L.co_tomo_fill(grid, n_angles, n_bins, _p(cos_t), _p(sin_t), _p(offs), _p(rp), _p(ci), _p(cv), nthreads)
+    trp = np.zeros(n + 1, dtype=np.int64)
+    tci = np.empty(nnz, dtype=np.int32)
+    tcv = np.empty(nnz, dtype=np.float32)
+    L.co_csr_transpose(m, n, _p(rp), _p(ci), _p(cv), _p(trp), _p(tci), _p(tcv), nthreads)
+    return (rp, ci, cv), (trp, tci, tcv), m, n
+
+
+def sparse_sign(ell, m, zeta, seed):
+    rng = np.random.default_rng(seed)
+    rows = np.argsort(rng.random((m, ell), dtype=np.float32), axis=1)[:, :zeta] if m * ell <= 5e7 else None
+    if rows is None:  # large: rejection-free approximate draw of distinct rows per column
+        rows = np.empty((m, zeta), dtype=np.int64)
+        base = rng.integers(0, ell, size=m)
+        steps = rng.integers(1, ell // zeta, size=(m, zeta))
+        rows = (base[:, None] + np.cumsum(steps, axis=1)) % ell
+    cols = np.repeat(np.arange(m), zeta)
+    vals = rng.choice([-1.0, 1.0], size=m * zeta) / math.sqrt(zeta)
+    S = scipy.sparse.csr_matrix((vals, (rows.ravel(), cols)), shape=(ell, m))
+    S.sum_duplicates()
+    return S
+
+
+def run_slslu(A, At, m, n, b, ell, maxiter, budget_s, nthreads, seed=7, S=None):
+    L = lib()
+    if S is None:
+        S = sparse_sign(ell, m, 8, seed)
+    Srp = np.ascontiguousarray(S.indptr, dtype=np.int64)
+    Sci = np.ascontiguousarray(S.indices, dtype=np.int32)
+    Scv = np.ascontiguousarray(S.data, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    t = np.zeros(maxiter + 1, dtype=np.int64)
+    g = np.zeros(maxiter + 1, dtype=np.int64)
+    sres = np.zeros(maxiter)
+    its = np.zeros(maxiter)
+    x = np.zeros(n)
+    done = L.co_slslu_f32(m, n, _p(A[0]), _p(A[1]), _p(A[2]), _p(At[0]), _p(At[1]), _p(At[2]), ell, _p(Srp), _p(Sci),
+                          _p(Scv), _p(b), maxiter, nthreads, budget_s, _p(t), _p(g), _p(sres), _p(its), _p(x))
+    return dict(done=done, t=t[: done + 1], g=g[: done + 1], sres=sres[:done], iter_s=its[:done], x=x)
+
+
+def extrapolate_rate(iter_s, K):
+    """iterations/s over a K-iteration run from t(k) = a + b k fitted to the sample."""
+    k = np.arange(1, len(iter_s) + 1, dtype=float)
+    if len(iter_s) >= 3:
+        A = np.vstack([np.ones_like(k[1:]), k[1:]]).T  # skip the first (cold) iteration
+        a, bb = np.linalg.lstsq(A, iter_s[1:], rcond=None)[0]
+        bb = max(bb, 0.0)
+    else:
+        a, bb = float(np.mean(iter_s)), 0.0
+    mean_t = a + bb * (K + 1) / 2.0
+    return 1.0 / mean_t, a, bb
+
+
+_cache = {}
+
+
+def host_problem(grid, angles, bins, seed, nthreads):
+    """Host-only copy of the tomography workload: operator, phantom, noisy b."""
+    from paper_2502_02721_b200.problems import add_noise, random_ellipses  # pure numpy input generators
+
+    key = (grid, angles, bins, seed)
+    if key not in _cache:
+        _cache.clear()
+        t0 = time.perf_counter()
+        A, At, m, n = host_tomography(grid, angles, bins, nthreads)
+        x = random_ellipses(grid, 10, seed).ravel()
+        bc = np.empty(m)
+        lib().co_spmv_f32_f64(m, _p(A[0]), _p(A[1]), _p(A[2]), _p(x), _p(bc), nthreads)
+        b, _ = add_noise(bc, 0.01, seed + 1)
+        _cache[key] = (A, At, m, n, x, b, time.perf_counter() - t0)
+    return _cache[key]
+
+
+def run(w, budget_s=20.0, nthreads=None, b=None):
+    """CPU baseline for a tomography Workload (paper_2502_02721_b200.problems)."""
+    nthreads = nthreads or os.cpu_count()
+    meta = w.meta
+    A, At, m, n, x, bh, build_s = host_problem(meta["grid"], meta["angles"], meta["bins"], 0, nthreads)
+    K = w.cfg.maxiter
+    r = run_slslu(A, At, m, n, bh if b is None else b, w.cfg.sketch_rows, K, budget_s, nthreads)
+    rate, a, bb = extrapolate_rate(r["iter_s"], K)
+    return {
+        "value": round(rate, 4),
+        "unit": "iterations/s",
+        "cores": nthreads,
+        "kind": "port",
+        "sample": (f"oracle/coracle.c (C port of solvers.py:410-539, fp32 vectors, OpenMP) on the full "
+                   f"{meta['grid']}^2 x {meta['angles']}x{meta['bins']} operator ({int(A[0][-1])} nnz, host-built): "
+                   f"{r['done']} of {K} iterations in {sum(r['iter_s']):.1f}s, rate extrapolated to {K} iterations "
+                   f"with t(k)={a:.3f}+{bb:.5f}k s; host operator build {build_s:.1f}s"),
+    }

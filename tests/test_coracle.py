@@ -1,0 +1,47 @@
+"""The C port of the reference loop (oracle/coracle.c, CPU baseline) against the
+numpy oracle: host-built tomography matrix bit-identical, pivots identical,
+iterates within rounding.  CPU only."""
+
+import numpy as np
+
+from oracle import cpu_baseline as cb
+from oracle import hessketch_oracle as ho
+from oracle import tomo_oracle as to
+
+
+def test_host_tomography_matches_oracle():
+    A, At, m, n = cb.host_tomography(40, 17, 31, 4)
+    K = to.tomography_matrix(40, 17, 31)
+    np.testing.assert_array_equal(A[0], K.indptr)
+    np.testing.assert_array_equal(A[1], K.indices)
+    np.testing.assert_array_equal(A[2], K.data.astype(np.float32))
+    Kt = K.T.tocsr()
+    np.testing.assert_array_equal(At[0], Kt.indptr)
+    np.testing.assert_array_equal(At[1], Kt.indices)
+    np.testing.assert_array_equal(At[2], Kt.data.astype(np.float32))
+
+
+def test_c_port_matches_oracle32():
+    from paper_2502_02721_b200.problems import add_noise, random_ellipses
+
+    grid, angles, bins = 48, 30, 69
+    A, At, m, n = cb.host_tomography(grid, angles, bins, 4)
+    K = to.tomography_matrix(grid, angles, bins)
+    x = random_ellipses(grid, 10, 0).ravel()
+    b, _ = add_noise(K @ x, 0.01, 1)
+    S = cb.sparse_sign(200, m, 8, 3)
+    r = cb.run_slslu(A, At, m, n, b, 200, 40, 1e9, 4, S=S)
+    ref = ho.hessenberg_solve(ho.csr_operator(K, np.float32), b, square=False, maxiter=40, S2=S, x_true=x)
+    t_ref, g_ref = ho.pivots_of(ref.state)
+    assert r["done"] == 40
+    np.testing.assert_array_equal(r["t"], t_ref)
+    np.testing.assert_array_equal(r["g"], g_ref)
+    np.testing.assert_allclose(r["sres"], ref.column("sres_norm"), rtol=1e-9)
+    assert np.linalg.norm(r["x"] - ref.x) <= 1e-9 * np.linalg.norm(ref.x)
+
+
+def test_rate_extrapolation():
+    its = 0.1 + 0.01 * np.arange(1, 21)
+    rate, a, b = cb.extrapolate_rate(its, 300)
+    assert abs(a - 0.1) < 1e-9 and abs(b - 0.01) < 1e-9
+    assert abs(rate - 1.0 / (0.1 + 0.01 * 150.5)) < 1e-9
