@@ -210,8 +210,34 @@ struct Csr {
 struct Sell {
   long long rows = 0, cols = 0, nnz = 0, slots = 0, nslices = 0;
   DBuf sptr, rlen, col, val;
-  bool ready() const { return nslices > 0 || rows == 0 ? sptr.p != nullptr : false; }
+  bool d16 = false;   // columns stored as int16 deltas (rbase + dcol) instead of col
+  DBuf rbase, dcol;
+  double index_bytes() const { return d16 ? 2.0 : 4.0; }
 };
+
+// Switch a SELL copy to 16-bit column deltas when every in-row step fits.
+static bool sell_try_delta16(hs_ctx* ctx, Sell& S) {
+  if (S.nslices == 0) return false;
+  cudaStream_t s = ctx->stream;
+  DBuf mx(sizeof(unsigned int));
+  sell_delta_range_kernel<<<grid_for(S.nslices, 8, 1 << 30), 256, 0, s>>>(
+      S.rows, S.nslices, S.sptr.as<long long>(), S.rlen.as<int>(), S.col.as<int>(), mx.as<unsigned int>());
+  CKL();
+  unsigned int h = 0;
+  CK(cudaMemcpyAsync(&h, mx.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (h > 32767u) return false;
+  S.rbase.alloc(std::max<long long>(S.rows, 1) * sizeof(int), false);
+  S.dcol.alloc(std::max<long long>(S.slots, 4) * sizeof(short), false);
+  sell_delta_fill_kernel<<<grid_for(S.nslices, 8, 1 << 30), 256, 0, s>>>(
+      S.rows, S.nslices, S.sptr.as<long long>(), S.rlen.as<int>(), S.col.as<int>(), S.rbase.as<int>(),
+      S.dcol.as<short>());
+  CKL();
+  CK(cudaStreamSynchronize(s));
+  S.col.release();
+  S.d16 = true;
+  return true;
+}
 
 template <class V>
 static void csr_to_sell(hs_ctx* ctx, const Csr& A, Sell& S) {
@@ -268,8 +294,10 @@ struct hs_op {
     if (kind == OP_CSR && (transpose ? Ats.nslices : As.nslices) > 0) {
       const Sell& M = transpose ? Ats : As;
       const int grid = grid_for(M.nslices, 8, ctx->num_sms * 16);
-      const double bytes = (double)M.nnz * (sizeof(V) + 4) + (double)M.rows * 4 + (double)M.nslices * 8 +
-                           (double)M.cols * sizeof(Tin) + (double)M.rows * sizeof(T);
+      // algorithmic bytes of the stored encoding: values + column indices (4 B, or 2 B deltas)
+      // + row lengths (+ row bases) + slice pointers + x once + y
+      const double bytes = (double)M.nnz * (sizeof(V) + M.index_bytes()) + (double)M.rows * (M.d16 ? 8 : 4) +
+                           (double)M.nslices * 8 + (double)M.cols * sizeof(Tin) + (double)M.rows * sizeof(T);
       const bool tflag = !transpose && sflag.p != nullptr;
       if (tflag) {
         // transposed image copy of x for the near-horizontal ray slices
@@ -281,10 +309,19 @@ struct hs_op {
         CKL();
       }
       Prof p(ctx, transpose ? "spmv_AT" : "spmv_A", bytes);
-      sell_spmv_kernel<V, Tin, T><<<grid, 256, 0, s>>>(M.rows, M.nslices, M.sptr.as<long long>(), M.rlen.as<int>(),
-                                                      M.col.as<int>(), M.val.as<V>(), xi,
-                                                      tflag ? xT.as<Tin>() : nullptr,
-                                                      tflag ? sflag.as<unsigned char>() : nullptr, yo);
+      if (M.d16) {
+        int gshift = -1;
+        if (img_grid > 0 && (img_grid & (img_grid - 1)) == 0) gshift = __builtin_ctz((unsigned)img_grid);
+        sell_spmv_d16_kernel<V, Tin, T><<<grid, 256, 0, s>>>(
+            M.rows, M.nslices, M.sptr.as<long long>(), M.rlen.as<int>(), M.rbase.as<int>(), M.dcol.as<short>(),
+            M.val.as<V>(), xi, tflag ? xT.as<Tin>() : nullptr, tflag ? sflag.as<unsigned char>() : nullptr, img_grid,
+            gshift, yo);
+      } else {
+        sell_spmv_kernel<V, Tin, T><<<grid, 256, 0, s>>>(M.rows, M.nslices, M.sptr.as<long long>(), M.rlen.as<int>(),
+                                                        M.col.as<int>(), M.val.as<V>(), xi,
+                                                        tflag ? xT.as<Tin>() : nullptr,
+                                                        tflag ? sflag.as<unsigned char>() : nullptr, yo);
+      }
       CKL();
     } else if (kind == OP_CSR) {
       const Csr& M = transpose ? At : A;
@@ -515,10 +552,11 @@ struct Solver {
             double* hcol) {
     if (k == 0) return;
     cudaStream_t s = ctx->stream;
-    if (k <= 8 * 32) fsub_warp_kernel<T, 8><<<1, 32, 0, s>>>(u, pos, 0, P, ldp, nullptr, k, st, iter, side, c, hcol);
-    else if (k <= 32 * 32)
-      fsub_warp_kernel<T, 32><<<1, 32, 0, s>>>(u, pos, 0, P, ldp, nullptr, k, st, iter, side, c, hcol);
-    else fail(HS_ERR_NOTIMPL, "maxiter above 1023 is not supported");
+    if (k <= 64) {
+      fsub_warp_kernel<T, 2><<<1, 32, 0, s>>>(u, pos, 0, P, ldp, nullptr, k, st, iter, side, c, hcol);
+    } else {
+      fsub_block_kernel<T><<<1, 512, (size_t)k * sizeof(T), s>>>(u, pos, 0, P, ldp, k, st, iter, side, c, hcol);
+    }
     CKL();
   }
 

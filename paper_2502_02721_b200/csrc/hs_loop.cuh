@@ -72,6 +72,57 @@ fsub_warp_kernel(const T* __restrict__ u, const long long* __restrict__ pos, lon
   }
 }
 
+// Blocked version (one CTA): the same per-row operation sequence
+//   v_j <- (((v_j - c_0 P_j0) - c_1 P_j1) - ...)   (i ascending)
+// organised in diagonal blocks of 32 unknowns.  Warp 0 solves a diagonal
+// block serially (its 32x32 slice of P prefetched into registers, c_i
+// broadcast by shuffle); then every thread applies the block's 32 new c_i to
+// the rows it owns, in i order.  Bit-identical to the serial loop, with a
+// critical path of ~k shuffles instead of k global-latency steps.
+template <class T>
+__global__ void __launch_bounds__(512)
+fsub_block_kernel(const T* __restrict__ u, const long long* __restrict__ pos, long long pos_offset,
+                  const T* __restrict__ P, int ldp, int k, const LoopState* __restrict__ st, int iter, int side,
+                  T* __restrict__ c, double* __restrict__ hcol) {
+  if (st->bd_iter != 0 && st->bd_iter < iter) return;
+  if (side == 1 && st->bd_iter == iter) return;
+  extern __shared__ unsigned char smem_raw[];
+  T* v = reinterpret_cast<T*>(smem_raw);  // k values
+  for (int j = threadIdx.x; j < k; j += blockDim.x) v[j] = u[pos[j] - pos_offset];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int b0 = 0; b0 < k; b0 += 32) {
+    const int nb = min(32, k - b0);
+    if (warp == 0) {
+      const int j = b0 + lane;
+      T Pd[32];
+#pragma unroll
+      for (int o = 0; o < 32; ++o) Pd[o] = (o < nb && j < k) ? P[(long long)(b0 + o) * ldp + j] : T(0);
+      T vj = j < k ? v[j] : T(0);
+#pragma unroll
+      for (int o = 0; o < 32; ++o) {
+        if (o < nb) {
+          const T co = __shfl_sync(0xffffffffu, vj, o);
+          if (lane > o && lane < nb) vj = Rn<T>::sub(vj, Rn<T>::mul(co, Pd[o]));
+        }
+      }
+      if (lane < nb) {
+        v[j] = vj;
+        c[j] = vj;
+        hcol[j] = (double)vj;
+      }
+    }
+    __syncthreads();
+    // rows below the block take the block's contributions in i order
+    for (int j = b0 + nb + threadIdx.x; j < k; j += blockDim.x) {
+      T vj = v[j];
+      for (int o = 0; o < nb; ++o) vj = Rn<T>::sub(vj, Rn<T>::mul(v[b0 + o], P[(long long)(b0 + o) * ldp + j]));
+      v[j] = vj;
+    }
+    __syncthreads();
+  }
+}
+
 // --------------------------------------------------------------------------
 // vector load helpers for the basis pass
 template <class B, int VEC> struct VecLoad;

@@ -308,10 +308,135 @@ __global__ void sell_transpose_cols_kernel(long long nslices, long long rows, in
   }
   const bool use_t = lines_t < lines_row;
   if (lane == 0) sflag[s] = use_t ? 1 : 0;
-  if (!use_t) return;
+  if (!use_t || n_bins < 0) return;  // n_bins < 0: choose only (columns stay in image order)
   for (long long p = sptr[s] + lane; p < sptr[s + 1]; p += 32) {
     const int c = col[p];
     col[p] = (c % grid) * grid + (c / grid);
+  }
+}
+
+// ---- 16-bit column deltas -------------------------------------------------------
+// Consecutive entries of a tomography row are neighbouring pixels (or rays), so
+// the column stream is stored as int16 differences plus one int32 base per
+// row: 6 instead of 8 bytes per nonzero from HBM.  Decoding is a running
+// integer sum per lane; values and the summation order are untouched.
+
+__global__ void sell_delta_range_kernel(long long rows, long long nslices, const long long* __restrict__ sptr,
+                                        const int* __restrict__ rlen, const int* __restrict__ col,
+                                        unsigned int* __restrict__ maxabs) {
+  const long long s = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (s >= nslices) return;
+  const int lane = threadIdx.x & 31;
+  const long long row = s * 32 + lane;
+  const int len = row < rows ? rlen[row] : 0;
+  const long long base = sptr[s];
+  unsigned int mx = 0;
+  int prev = 0;
+  for (int e = 0; e < len; ++e) {
+    const int c = col[base + (long long)(e >> 2) * 128 + lane * 4 + (e & 3)];
+    if (e > 0) {
+      const long long d = (long long)c - prev;
+      const unsigned int a = (unsigned int)(d < 0 ? -d : d);
+      mx = a > mx ? a : mx;
+    }
+    prev = c;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) atomicMax(maxabs, mx);
+}
+
+__global__ void sell_delta_fill_kernel(long long rows, long long nslices, const long long* __restrict__ sptr,
+                                       const int* __restrict__ rlen, const int* __restrict__ col,
+                                       int* __restrict__ rbase, short* __restrict__ dcol) {
+  const long long s = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (s >= nslices) return;
+  const int lane = threadIdx.x & 31;
+  const long long row = s * 32 + lane;
+  const int len = row < rows ? rlen[row] : 0;
+  const long long base = sptr[s];
+  const int nslots = (int)((sptr[s + 1] - base) >> 7) * 4;
+  int prev = 0;
+  for (int e = 0; e < nslots; ++e) {
+    const long long slot = base + (long long)(e >> 2) * 128 + lane * 4 + (e & 3);
+    short d = 0;
+    if (e < len) {
+      const int c = col[slot];
+      if (e == 0) {
+        if (row < rows) rbase[row] = c;
+      } else {
+        d = (short)(c - prev);
+      }
+      prev = c;
+    }
+    dcol[slot] = d;
+  }
+  if (len == 0 && row < rows) rbase[row] = 0;
+}
+
+template <class Tin>
+__device__ __forceinline__ const Tin* pick_x(const Tin* xrow, const Tin* xT, const unsigned char* sflag, long long s) {
+  return (sflag != nullptr && sflag[s]) ? xT : xrow;
+}
+
+// column index in the gathered vector: image order, or transposed for flagged slices
+__device__ __forceinline__ int tidx(int c, bool tr, int grid, int gshift) {
+  if (!tr) return c;
+  if (gshift >= 0) return ((c & (grid - 1)) << gshift) | (c >> gshift);
+  return (c % grid) * grid + c / grid;
+}
+
+template <class V, class Tin, class T>
+__global__ void __launch_bounds__(256)
+sell_spmv_d16_kernel(long long rows, long long nslices, const long long* __restrict__ sptr,
+                     const int* __restrict__ rlen, const int* __restrict__ rbase, const short* __restrict__ dcol,
+                     const V* __restrict__ val, const Tin* __restrict__ xrow, const Tin* __restrict__ xT,
+                     const unsigned char* __restrict__ sflag, int grid, int gshift, T* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const long long wstride = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long s = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); s < nslices; s += wstride) {
+    const bool tr = sflag != nullptr && sflag[s];
+    const Tin* __restrict__ x = tr ? xT : xrow;
+    const long long row = s * 32 + lane;
+    int len = 0, c = 0;
+    if (row < rows) {
+      len = rlen[row];
+      c = rbase[row];
+    }
+    const long long base = sptr[s];
+    const int nq = (len + 3) >> 2;
+    const short* dp = dcol + base + lane * 4;
+    const V* vp = val + base + lane * 4;
+    T acc = T(0);
+    if (nq > 0) {
+      int2 d = __ldcs(reinterpret_cast<const int2*>(dp));
+      Chunk4<V> v = Chunk4<V>::load(vp);
+      for (int q = 0; q < nq; ++q) {
+        int2 dn = d;
+        Chunk4<V> vn = v;
+        if (q + 1 < nq) {
+          dn = __ldcs(reinterpret_cast<const int2*>(dp + (long long)(q + 1) * 128));
+          vn = Chunk4<V>::load(vp + (long long)(q + 1) * 128);
+        }
+        const int e = q * 4;
+        const int c0 = c + (int)(short)(d.x & 0xffff);
+        const int c1 = c0 + (int)(short)(d.x >> 16);
+        const int c2 = c1 + (int)(short)(d.y & 0xffff);
+        const int c3 = c2 + (int)(short)(d.y >> 16);
+        const T x0 = gather_x<T>(x, tidx(c0, tr, grid, gshift));
+        const T x1 = (e + 1 < len) ? gather_x<T>(x, tidx(c1, tr, grid, gshift)) : T(0);
+        const T x2 = (e + 2 < len) ? gather_x<T>(x, tidx(c2, tr, grid, gshift)) : T(0);
+        const T x3 = (e + 3 < len) ? gather_x<T>(x, tidx(c3, tr, grid, gshift)) : T(0);
+        acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[0]), x0));
+        if (e + 1 < len) acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[1]), x1));
+        if (e + 2 < len) acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[2]), x2));
+        if (e + 3 < len) acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[3]), x3));
+        c = c3;
+        d = dn;
+        v = vn;
+      }
+    }
+    if (row < rows) y[row] = acc;
   }
 }
 
