@@ -210,6 +210,8 @@ struct Csr {
 struct Sell {
   long long rows = 0, cols = 0, nnz = 0, slots = 0, nslices = 0;
   DBuf sptr, rlen, col, val;
+  DBuf rperm;         // optional slot -> row map (slots are nslices*32; -1 = empty)
+  long long nslots() const { return nslices * 32; }
   bool d16 = false;   // columns stored as int16 deltas (rbase + dcol) instead of col
   DBuf rbase, dcol;
   double index_bytes() const { return d16 ? 2.0 : 4.0; }
@@ -221,16 +223,16 @@ static bool sell_try_delta16(hs_ctx* ctx, Sell& S) {
   cudaStream_t s = ctx->stream;
   DBuf mx(sizeof(unsigned int));
   sell_delta_range_kernel<<<grid_for(S.nslices, 8, 1 << 30), 256, 0, s>>>(
-      S.rows, S.nslices, S.sptr.as<long long>(), S.rlen.as<int>(), S.col.as<int>(), mx.as<unsigned int>());
+      S.nslots(), S.nslices, S.sptr.as<long long>(), S.rlen.as<int>(), S.col.as<int>(), mx.as<unsigned int>());
   CKL();
   unsigned int h = 0;
   CK(cudaMemcpyAsync(&h, mx.p, sizeof(h), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   if (h > 32767u) return false;
-  S.rbase.alloc(std::max<long long>(S.rows, 1) * sizeof(int), false);
+  S.rbase.alloc(std::max<long long>(S.nslots(), 1) * sizeof(int), false);
   S.dcol.alloc(std::max<long long>(S.slots, 4) * sizeof(short), false);
   sell_delta_fill_kernel<<<grid_for(S.nslices, 8, 1 << 30), 256, 0, s>>>(
-      S.rows, S.nslices, S.sptr.as<long long>(), S.rlen.as<int>(), S.col.as<int>(), S.rbase.as<int>(),
+      S.nslots(), S.nslices, S.sptr.as<long long>(), S.rlen.as<int>(), S.col.as<int>(), S.rbase.as<int>(),
       S.dcol.as<short>());
   CKL();
   CK(cudaStreamSynchronize(s));
@@ -239,17 +241,26 @@ static bool sell_try_delta16(hs_ctx* ctx, Sell& S) {
   return true;
 }
 
+// tile_grid > 0: slots follow 8x4 pixel tiles of a tile_grid^2 image (rows = pixels)
 template <class V>
-static void csr_to_sell(hs_ctx* ctx, const Csr& A, Sell& S) {
+static void csr_to_sell(hs_ctx* ctx, const Csr& A, Sell& S, int tile_grid = 0) {
   cudaStream_t s = ctx->stream;
   S.rows = A.rows;
   S.cols = A.cols;
   S.nnz = A.nnz;
-  S.nslices = (A.rows + 31) / 32;
-  S.rlen.alloc(std::max<long long>(A.rows, 1) * sizeof(int), false);
+  if (tile_grid > 0) {
+    const long long tiles = (long long)((tile_grid + 7) / 8) * ((tile_grid + 3) / 4);
+    S.nslices = tiles;
+    S.rperm.alloc(S.nslots() * sizeof(int), false);
+    tile_perm_kernel<<<grid_for(S.nslots(), 256, 1 << 30), 256, 0, s>>>(tile_grid, S.nslots(), S.rperm.as<int>());
+    CKL();
+  } else {
+    S.nslices = (A.rows + 31) / 32;
+  }
+  S.rlen.alloc(std::max<long long>(S.nslots(), 1) * sizeof(int), false);
   DBuf slots((S.nslices + 1) * sizeof(long long));
   sell_slice_chunks_kernel<<<grid_for(S.nslices, 8, 1 << 30), 256, 0, s>>>(
-      A.rows, S.nslices, A.rowptr.as<long long>(), S.rlen.as<int>(), slots.as<long long>());
+      A.rows, S.nslices, A.rowptr.as<long long>(), S.rperm.as<int>(), S.rlen.as<int>(), slots.as<long long>());
   CKL();
   S.sptr.alloc((S.nslices + 1) * sizeof(long long), false);
   size_t tmp = 0;
@@ -261,8 +272,8 @@ static void csr_to_sell(hs_ctx* ctx, const Csr& A, Sell& S) {
   S.col.alloc(std::max<long long>(S.slots, 4) * sizeof(int), false);
   S.val.alloc(std::max<long long>(S.slots, 4) * sizeof(V), false);
   sell_fill_kernel<V><<<grid_for(S.nslices, 8, 1 << 30), 256, 0, s>>>(
-      A.rows, S.nslices, A.rowptr.as<long long>(), A.col.as<int>(), A.val.as<V>(), S.sptr.as<long long>(),
-      S.col.as<int>(), S.val.as<V>());
+      A.rows, S.nslices, A.rowptr.as<long long>(), S.rperm.as<int>(), A.col.as<int>(), A.val.as<V>(),
+      S.sptr.as<long long>(), S.col.as<int>(), S.val.as<V>());
   CKL();
   CK(cudaStreamSynchronize(s));
 }
@@ -312,15 +323,17 @@ struct hs_op {
       if (M.d16) {
         int gshift = -1;
         if (img_grid > 0 && (img_grid & (img_grid - 1)) == 0) gshift = __builtin_ctz((unsigned)img_grid);
-        sell_spmv_d16_kernel<V, Tin, T><<<grid, 256, 0, s>>>(
-            M.rows, M.nslices, M.sptr.as<long long>(), M.rlen.as<int>(), M.rbase.as<int>(), M.dcol.as<short>(),
-            M.val.as<V>(), xi, tflag ? xT.as<Tin>() : nullptr, tflag ? sflag.as<unsigned char>() : nullptr, img_grid,
-            gshift, yo);
+        auto kern = (gshift >= 0 || !tflag) ? sell_spmv_d16_kernel<V, Tin, T, true> : sell_spmv_d16_kernel<V, Tin, T, false>;
+        kern<<<grid, 256, 0, s>>>(M.rows, M.nslices, M.sptr.as<long long>(), M.rlen.as<int>(), M.rbase.as<int>(),
+                                  M.dcol.as<short>(), M.val.as<V>(), xi, tflag ? xT.as<Tin>() : nullptr,
+                                  tflag ? sflag.as<unsigned char>() : nullptr, img_grid, gshift >= 0 ? gshift : 0,
+                                  M.rperm.as<int>(), yo);
       } else {
         sell_spmv_kernel<V, Tin, T><<<grid, 256, 0, s>>>(M.rows, M.nslices, M.sptr.as<long long>(), M.rlen.as<int>(),
                                                         M.col.as<int>(), M.val.as<V>(), xi,
                                                         tflag ? xT.as<Tin>() : nullptr,
-                                                        tflag ? sflag.as<unsigned char>() : nullptr, yo);
+                                                        tflag ? sflag.as<unsigned char>() : nullptr,
+                                                        M.rperm.as<int>(), yo);
       }
       CKL();
     } else if (kind == OP_CSR) {

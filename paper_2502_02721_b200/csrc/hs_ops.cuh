@@ -211,13 +211,14 @@ __global__ void __launch_bounds__(256)
 sell_spmv_kernel(long long rows, long long nslices, const long long* __restrict__ sptr,
                  const int* __restrict__ rlen, const int* __restrict__ col, const V* __restrict__ val,
                  const Tin* __restrict__ xrow, const Tin* __restrict__ xT, const unsigned char* __restrict__ sflag,
-                 T* __restrict__ y) {
+                 const int* __restrict__ rperm, T* __restrict__ y) {
   const int lane = threadIdx.x & 31;
   const long long wstride = (long long)gridDim.x * (blockDim.x >> 5);
   for (long long s = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); s < nslices; s += wstride) {
     const Tin* __restrict__ x = (sflag != nullptr && sflag[s]) ? xT : xrow;
-    const long long row = s * 32 + lane;
-    const int len = row < rows ? rlen[row] : 0;
+    const long long slot = s * 32 + lane;  // rlen / rbase are slot-indexed; rperm maps slot -> row
+    const long long row = rperm ? (long long)rperm[slot] : slot;
+    const int len = rlen[slot];
     const long long base = sptr[s];
     const int nq_slice = (int)((sptr[s + 1] - base) >> 7);
     const int nq = (len + 3) >> 2;
@@ -250,7 +251,7 @@ sell_spmv_kernel(long long rows, long long nslices, const long long* __restrict_
       }
     }
     (void)nq_slice;
-    if (row < rows) y[row] = acc;
+    if (row >= 0 && row < rows) y[row] = acc;
   }
 }
 
@@ -386,73 +387,114 @@ __device__ __forceinline__ int tidx(int c, bool tr, int grid, int gshift) {
   return (c % grid) * grid + c / grid;
 }
 
-template <class V, class Tin, class T>
-__global__ void __launch_bounds__(256)
+// gather index of column c: identity, or the transposed-image position.
+// POW2 (grid = 2^sh): branch-free  ((c & m) << sh) | (c >> sh)  with
+// (m, sh) = (-1, 0) for image-order slices and (grid-1, log2 grid) otherwise.
+template <bool POW2>
+__device__ __forceinline__ int gidx(int c, int m, int sh, bool tr, int grid) {
+  if (POW2) return ((c & m) << sh) | (c >> sh);
+  return tr ? (c % grid) * grid + c / grid : c;
+}
+
+template <class V, class Tin, class T, bool POW2>
+__global__ void __launch_bounds__(256, (sizeof(T) == 4 && sizeof(V) == 4) ? 6 : 3)
 sell_spmv_d16_kernel(long long rows, long long nslices, const long long* __restrict__ sptr,
                      const int* __restrict__ rlen, const int* __restrict__ rbase, const short* __restrict__ dcol,
                      const V* __restrict__ val, const Tin* __restrict__ xrow, const Tin* __restrict__ xT,
-                     const unsigned char* __restrict__ sflag, int grid, int gshift, T* __restrict__ y) {
+                     const unsigned char* __restrict__ sflag, int grid, int gshift, const int* __restrict__ rperm,
+                     T* __restrict__ y) {
   const int lane = threadIdx.x & 31;
   const long long wstride = (long long)gridDim.x * (blockDim.x >> 5);
   for (long long s = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); s < nslices; s += wstride) {
     const bool tr = sflag != nullptr && sflag[s];
     const Tin* __restrict__ x = tr ? xT : xrow;
-    const long long row = s * 32 + lane;
-    int len = 0, c = 0;
-    if (row < rows) {
-      len = rlen[row];
-      c = rbase[row];
-    }
+    const int m = tr ? grid - 1 : -1, sh = tr ? gshift : 0;
+    const long long slot = s * 32 + lane;  // rlen / rbase are slot-indexed; rperm maps slot -> row
+    const long long row = rperm ? (long long)rperm[slot] : slot;
+    const int len = rlen[slot];
+    int c = rbase[slot];
     const long long base = sptr[s];
-    const int nq = (len + 3) >> 2;
+    const int nq = (len + 3) >> 2, nfull = len >> 2;
     const short* dp = dcol + base + lane * 4;
     const V* vp = val + base + lane * 4;
     T acc = T(0);
     if (nq > 0) {
+      // one chunk of (delta, value) prefetched ahead; gathers issued as soon
+      // as a chunk's columns are decoded (a deeper per-lane pipeline costs
+      // registers, i.e. resident warps, and measured slower)
       int2 d = __ldcs(reinterpret_cast<const int2*>(dp));
       Chunk4<V> v = Chunk4<V>::load(vp);
-      for (int q = 0; q < nq; ++q) {
+      // full chunks: no per-entry predicates
+      for (int q = 0; q < nfull; ++q) {
         int2 dn = d;
         Chunk4<V> vn = v;
         if (q + 1 < nq) {
           dn = __ldcs(reinterpret_cast<const int2*>(dp + (long long)(q + 1) * 128));
           vn = Chunk4<V>::load(vp + (long long)(q + 1) * 128);
         }
-        const int e = q * 4;
         const int c0 = c + (int)(short)(d.x & 0xffff);
-        const int c1 = c0 + (int)(short)(d.x >> 16);
+        const int c1 = c0 + (d.x >> 16);
         const int c2 = c1 + (int)(short)(d.y & 0xffff);
-        const int c3 = c2 + (int)(short)(d.y >> 16);
-        const T x0 = gather_x<T>(x, tidx(c0, tr, grid, gshift));
-        const T x1 = (e + 1 < len) ? gather_x<T>(x, tidx(c1, tr, grid, gshift)) : T(0);
-        const T x2 = (e + 2 < len) ? gather_x<T>(x, tidx(c2, tr, grid, gshift)) : T(0);
-        const T x3 = (e + 3 < len) ? gather_x<T>(x, tidx(c3, tr, grid, gshift)) : T(0);
+        const int c3 = c2 + (d.y >> 16);
+        const T x0 = gather_x<T>(x, gidx<POW2>(c0, m, sh, tr, grid));
+        const T x1 = gather_x<T>(x, gidx<POW2>(c1, m, sh, tr, grid));
+        const T x2 = gather_x<T>(x, gidx<POW2>(c2, m, sh, tr, grid));
+        const T x3 = gather_x<T>(x, gidx<POW2>(c3, m, sh, tr, grid));
         acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[0]), x0));
-        if (e + 1 < len) acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[1]), x1));
-        if (e + 2 < len) acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[2]), x2));
-        if (e + 3 < len) acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[3]), x3));
+        acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[1]), x1));
+        acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[2]), x2));
+        acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[3]), x3));
         c = c3;
         d = dn;
         v = vn;
       }
+      const int rem = len & 3;
+      if (rem) {  // tail chunk (already loaded into d / v)
+        const int c0 = c + (int)(short)(d.x & 0xffff);
+        const int c1 = c0 + (d.x >> 16);
+        const int c2 = c1 + (int)(short)(d.y & 0xffff);
+        acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[0]), gather_x<T>(x, gidx<POW2>(c0, m, sh, tr, grid))));
+        if (rem > 1) acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[1]), gather_x<T>(x, gidx<POW2>(c1, m, sh, tr, grid))));
+        if (rem > 2) acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[2]), gather_x<T>(x, gidx<POW2>(c2, m, sh, tr, grid))));
+      }
     }
-    if (row < rows) y[row] = acc;
+    if (row >= 0 && row < rows) y[row] = acc;
   }
 }
 
+// slot permutation grouping an image's pixels into 8-wide x 4-tall tiles
+// (one tile per slice): used for A^T, whose 32 lanes then hit the same few
+// detectors at every angle instead of a 32-pixel image row's wider shadow
+__global__ void tile_perm_kernel(int grid, long long nslots, int* __restrict__ rperm) {
+  const long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= nslots) return;
+  const int tiles_x = (grid + 7) / 8;
+  const long long tile = slot >> 5;
+  const int lane = (int)(slot & 31);
+  const long long ty = tile / tiles_x, tx = tile % tiles_x;
+  const long long r = ty * 4 + (lane >> 3), c = tx * 8 + (lane & 7);
+  rperm[slot] = (r < grid && c < grid) ? (int)(r * grid + c) : -1;
+}
+
 // ---- CSR -> SELL-32x4 conversion ------------------------------------------------
+// Slot s*32+lane holds row rperm[slot] (or row = slot without a permutation;
+// rperm < 0 marks an empty padding slot).  rlen is slot-indexed.
+__device__ __forceinline__ long long slot_row(const int* rperm, long long slot, long long rows) {
+  const long long r = rperm ? (long long)rperm[slot] : slot;
+  return (r >= 0 && r < rows) ? r : -1;
+}
+
 // per slice: number of 4-entry chunks of its longest row
 __global__ void sell_slice_chunks_kernel(long long rows, long long nslices, const long long* __restrict__ rowptr,
-                                         int* __restrict__ rlen, long long* __restrict__ slice_slots) {
+                                         const int* __restrict__ rperm, int* __restrict__ rlen,
+                                         long long* __restrict__ slice_slots) {
   const long long s = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (s >= nslices) return;
   const int lane = threadIdx.x & 31;
-  const long long row = s * 32 + lane;
+  const long long row = slot_row(rperm, s * 32 + lane, rows);
   int len = 0;
-  if (row < rows) {
-    len = (int)(rowptr[row + 1] - rowptr[row]);
-    rlen[row] = len;
-  }
+  if (row >= 0) len = (int)(rowptr[row + 1] - rowptr[row]);
+  rlen[s * 32 + lane] = len;
   int nq = (len + 3) >> 2;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) nq = max(nq, __shfl_xor_sync(0xffffffffu, nq, o));
@@ -461,17 +503,18 @@ __global__ void sell_slice_chunks_kernel(long long rows, long long nslices, cons
 
 template <class V>
 __global__ void sell_fill_kernel(long long rows, long long nslices, const long long* __restrict__ rowptr,
-                                 const int* __restrict__ ccol, const V* __restrict__ cval,
-                                 const long long* __restrict__ sptr, int* __restrict__ scol, V* __restrict__ sval) {
+                                 const int* __restrict__ rperm, const int* __restrict__ ccol,
+                                 const V* __restrict__ cval, const long long* __restrict__ sptr,
+                                 int* __restrict__ scol, V* __restrict__ sval) {
   const long long s = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (s >= nslices) return;
   const int lane = threadIdx.x & 31;
-  const long long row = s * 32 + lane;
+  const long long row = slot_row(rperm, s * 32 + lane, rows);
   const long long base = sptr[s];
   const int nslots = (int)((sptr[s + 1] - base) >> 7) * 4;  // entries per row incl. padding
   long long r0 = 0;
   int len = 0;
-  if (row < rows) {
+  if (row >= 0) {
     r0 = rowptr[row];
     len = (int)(rowptr[row + 1] - r0);
   }
