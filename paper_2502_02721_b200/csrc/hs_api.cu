@@ -211,6 +211,7 @@ struct Sell {
   long long rows = 0, cols = 0, nnz = 0, slots = 0, nslices = 0;
   DBuf sptr, rlen, col, val;
   DBuf rperm;         // optional slot -> row map (slots are nslices*32; -1 = empty)
+  DBuf sorder, sched; // slices longest-first + the dynamic scheduler's two counters
   long long nslots() const { return nslices * 32; }
   bool d16 = false;   // columns stored as int16 deltas (rbase + dcol) instead of col
   DBuf rbase, dcol;
@@ -269,6 +270,22 @@ static void csr_to_sell(hs_ctx* ctx, const Csr& A, Sell& S, int tile_grid = 0) {
   CK(cub::DeviceScan::ExclusiveSum(t.p, tmp, slots.as<long long>(), S.sptr.as<long long>(), S.nslices + 1, s));
   CK(cudaMemcpyAsync(&S.slots, S.sptr.as<long long>() + S.nslices, sizeof(long long), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  {  // longest-first slice order for the dynamic scheduler
+    DBuf sz(S.nslices * sizeof(unsigned int), false), szo(S.nslices * sizeof(unsigned int), false),
+        id(S.nslices * sizeof(int), false);
+    S.sorder.alloc(S.nslices * sizeof(int), false);
+    S.sched.alloc(2 * sizeof(unsigned int), true);
+    sell_slice_size_kernel<<<grid_for(S.nslices, 256, 1 << 30), 256, 0, s>>>(S.nslices, S.sptr.as<long long>(),
+                                                                             sz.as<unsigned int>(), id.as<int>());
+    CKL();
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, sz.as<unsigned int>(), szo.as<unsigned int>(),
+                                                 id.as<int>(), S.sorder.as<int>(), (int)S.nslices, 0, 32, s));
+    DBuf tt(tb, false);
+    CK(cub::DeviceRadixSort::SortPairsDescending(tt.p, tb, sz.as<unsigned int>(), szo.as<unsigned int>(),
+                                                 id.as<int>(), S.sorder.as<int>(), (int)S.nslices, 0, 32, s));
+    CK(cudaStreamSynchronize(s));
+  }
   S.col.alloc(std::max<long long>(S.slots, 4) * sizeof(int), false);
   S.val.alloc(std::max<long long>(S.slots, 4) * sizeof(V), false);
   sell_fill_kernel<V><<<grid_for(S.nslices, 8, 1 << 30), 256, 0, s>>>(
@@ -327,7 +344,8 @@ struct hs_op {
         kern<<<grid, 256, 0, s>>>(M.rows, M.nslices, M.sptr.as<long long>(), M.rlen.as<int>(), M.rbase.as<int>(),
                                   M.dcol.as<short>(), M.val.as<V>(), xi, tflag ? xT.as<Tin>() : nullptr,
                                   tflag ? sflag.as<unsigned char>() : nullptr, img_grid, gshift >= 0 ? gshift : 0,
-                                  M.rperm.as<int>(), yo);
+                                  M.rperm.as<int>(), transpose ? nullptr : M.sorder.as<int>(),
+                                  M.sched.as<unsigned int>(), yo);
       } else {
         sell_spmv_kernel<V, Tin, T><<<grid, 256, 0, s>>>(M.rows, M.nslices, M.sptr.as<long long>(), M.rlen.as<int>(),
                                                         M.col.as<int>(), M.val.as<V>(), xi,
@@ -588,7 +606,6 @@ struct Solver {
     const int Ls = (int)(lamon ? 2 * ell : ell);
     const int ldq = (int)round_up(Ls, 32);
     const int SMS = ctx->num_sms;
-    const int ELIM_CAP = SMS * 8;
 
     // ---- buffers
     auto Lb = std::make_shared<DBuf>((size_t)(K + 1) * ldn * sizeof(B));
@@ -607,7 +624,8 @@ struct Solver {
     const int NB = std::max(1, std::min(64, (Ls + 47) / 48));
     DBuf part((size_t)4 * NB * (K + 2) * sizeof(double));
     DBuf sresb(K * sizeof(double)), projb(K * sizeof(double)), rfb(K * sizeof(int)), rel2((K + 1) * sizeof(double));
-    DBuf candp((size_t)std::max(ELIM_CAP, 4096) * sizeof(Cand)), xpart((size_t)std::max(ELIM_CAP, 4096) * sizeof(double));
+    const int CAND_CAP = (int)std::min<long long>(1LL << 20, std::max<long long>(4096, (std::max(ldm, ldn) / VEC + 255) / 256));
+    DBuf candp((size_t)CAND_CAP * sizeof(Cand)), xpart((size_t)CAND_CAP * sizeof(double));
     DBuf stb(sizeof(LoopState));
     st = stb.as<LoopState>();
     LoopState hst;
@@ -752,15 +770,15 @@ struct Solver {
     auto elim = [&](T* vec, long long len, long long ldv, const B* basis, int k, int side, int iter, int kx,
                     const double* yx, double* relerr_slot) {
       const long long nvec = (len + VEC - 1) / VEC;
-      const int g = grid_for(nvec, 256, ELIM_CAP);
+      const int g = grid_for(nvec, 256, CAND_CAP);
       const size_t smem = ((k * sizeof(T) + 15) / 16) * 16 + (size_t)kx * sizeof(double) + elim_smem_base;
       const double bytes = (double)std::max(k, kx) * len * sizeof(B) + 2.0 * len * sizeof(T) +
                            (kx ? (double)len * 8 : 0.0);
       Prof p(ctx, side == 0 && !square ? "elim_D" : "elim_L", bytes);
-      if (smem > 48 * 1024)
-        CK(cudaFuncSetAttribute(elim_pass_kernel<T, B, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      auto kern = kx ? elim_pass_kernel<T, B, VEC, true> : elim_pass_kernel<T, B, VEC, false>;
+      if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       (void)ldv;
-      elim_pass_kernel<T, B, VEC><<<g, 256, smem, s>>>(
+      kern<<<g, 256, smem, s>>>(
           len, 0, basis, square || side == 1 ? ldn : ldm, nullptr, k, cvec.as<T>(), vec, kx, yx, nullptr,
           x0_h ? x0d.as<double>() : nullptr, kx ? xtd.as<double>() : nullptr, xpart.as<double>(), relerr_slot,
           candp.as<Cand>(), st, side, iter, 1);

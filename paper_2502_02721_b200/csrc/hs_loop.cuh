@@ -153,7 +153,7 @@ template <> struct VecLoad<__nv_bfloat16, 8> {
 //   x[e]  = x0[e] + sum_{j<kx} y_j b_j[e]                  (optional, fp64)
 // plus argmax |u'| and sum (x - x_true)^2 partials; the last block to finish
 // reduces the partials (fixed order) into st->piv_* / relerr slot.
-template <class T, class B, int VEC>
+template <class T, class B, int VEC, bool XF>
 __global__ void __launch_bounds__(256)
 elim_pass_kernel(long long n, long long idx_offset, const B* __restrict__ basis, long long ld,
                  const int* __restrict__ kptr, int kfixed, const T* __restrict__ cvec, T* __restrict__ u,
@@ -178,31 +178,33 @@ elim_pass_kernel(long long n, long long idx_offset, const B* __restrict__ basis,
   Cand best{-1.0, 0.0, 0x7fffffffffffffffLL};
   double sq = 0.0;
   const long long nvec = (n + VEC - 1) / VEC;
+  // one VEC-wide strip per thread (grid covers the vector exactly: no tail wave)
   for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < nvec;
        v += (long long)gridDim.x * blockDim.x) {
     const long long e0 = v * VEC;
     T acc[VEC];
-    double xa[VEC];
+    T xa[VEC];  // fused iterate of the previous iteration: accumulated in T (fp32 FMA in the
+                // fp32 path: converting every basis value to fp64 would bind the pass to the
+                // FP64 pipe; the final x is recomputed in fp64 by xpass_kernel)
 #pragma unroll
     for (int q = 0; q < VEC; ++q) {
       acc[q] = (e0 + q < n) ? u[e0 + q] : T(0);
-      xa[q] = 0.0;
+      xa[q] = T(0);
     }
     const B* bp = basis + e0;
-    const int kk = k > kx ? k : kx;
-#pragma unroll 4
-    for (int j = 0; j < kk; ++j) {
+    // kx <= k always (x of the previous iteration uses the first k-1 columns)
+    constexpr int UNR = XF ? 4 : 8;
+#pragma unroll UNR
+    for (int j = 0; j < k; ++j) {
       B b[VEC];
       VecLoad<B, VEC>::ld(bp + (long long)j * ld, b);
-      if (j < k) {
-        const T cj = cs[j];
+      const T cj = cs[j];
 #pragma unroll
-        for (int q = 0; q < VEC; ++q) acc[q] = Rn<T>::sub(acc[q], Rn<T>::mul(cj, cvt<T>(b[q])));
-      }
-      if (j < kx) {
-        const double yj = ys[j];
+      for (int q = 0; q < VEC; ++q) acc[q] = Rn<T>::sub(acc[q], Rn<T>::mul(cj, cvt<T>(b[q])));
+      if (XF && j < kx) {
+        const T yj = (T)ys[j];
 #pragma unroll
-        for (int q = 0; q < VEC; ++q) xa[q] = fma(yj, cvt<double>(b[q]), xa[q]);
+        for (int q = 0; q < VEC; ++q) xa[q] = fma(yj, cvt<T>(b[q]), xa[q]);
       }
     }
 #pragma unroll
@@ -212,8 +214,8 @@ elim_pass_kernel(long long n, long long idx_offset, const B* __restrict__ basis,
         if (write_u) u[e] = acc[q];
         const double mg = (double)absval(acc[q]);
         if (better(mg, idx_offset + e, best.mag, best.idx)) best = Cand{mg, (double)acc[q], idx_offset + e};
-        if (kx > 0) {
-          double xe = xa[q] + (x0 ? x0[e] : 0.0);
+        if (XF && kx > 0) {
+          double xe = (double)xa[q] + (x0 ? x0[e] : 0.0);
           if (xout) xout[e] = xe;
           if (xt) {
             const double d = xe - xt[e];
@@ -224,10 +226,10 @@ elim_pass_kernel(long long n, long long idx_offset, const B* __restrict__ basis,
     }
   }
   best = block_argmax(best, scratch);
-  if (kx > 0 && xt) sq = block_sum(sq, dscratch);
+  if (XF && kx > 0 && xt) sq = block_sum(sq, dscratch);
   if (threadIdx.x == 0) {
     cand_part[blockIdx.x] = best;
-    if (kx > 0 && xt) xpart[blockIdx.x] = sq;
+    if (XF && kx > 0 && xt) xpart[blockIdx.x] = sq;
     __threadfence();
     const unsigned prev = atomicAdd(&st->counter[side], 1u);
     am_last = (prev == gridDim.x - 1);
@@ -244,10 +246,12 @@ elim_pass_kernel(long long n, long long idx_offset, const B* __restrict__ basis,
     cand_merge(b2, c);
   }
   b2 = block_argmax(b2, scratch);
-  if (kx > 0 && xt && relerr_out && threadIdx.x == 0) {
+  if (XF && kx > 0 && xt && relerr_out) {
+    // fixed-order parallel sum of the block partials (deterministic)
     double s = 0.0;
-    for (int i = 0; i < (int)gridDim.x; ++i) s += __ldcg(&xpart[i]);
-    *relerr_out = s;  // squared norm; the host-side finalisation divides by |x_true|
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) s += __ldcg(&xpart[i]);
+    s = block_sum(s, dscratch);
+    if (threadIdx.x == 0) *relerr_out = s;  // squared norm; the host divides by |x_true|
   }
   if (threadIdx.x == 0) {
     st->piv_val[side] = b2.val;
@@ -379,9 +383,10 @@ xpass_kernel(long long n, const B* __restrict__ basis, long long ld, int kx, con
   __syncthreads();
   if (!am_last) return;
   __threadfence();
+  double s = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) s += __ldcg(&xpart[i]);
+  s = block_sum(s, dscratch);
   if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int i = 0; i < (int)gridDim.x; ++i) s += __ldcg(&xpart[i]);
     *relerr_out = s;
     st->counter[2] = 0;
   }

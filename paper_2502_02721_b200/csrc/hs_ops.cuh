@@ -402,10 +402,16 @@ sell_spmv_d16_kernel(long long rows, long long nslices, const long long* __restr
                      const int* __restrict__ rlen, const int* __restrict__ rbase, const short* __restrict__ dcol,
                      const V* __restrict__ val, const Tin* __restrict__ xrow, const Tin* __restrict__ xT,
                      const unsigned char* __restrict__ sflag, int grid, int gshift, const int* __restrict__ rperm,
-                     T* __restrict__ y) {
+                     const int* __restrict__ sorder, unsigned int* __restrict__ sched, T* __restrict__ y) {
   const int lane = threadIdx.x & 31;
-  const long long wstride = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long s = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); s < nslices; s += wstride) {
+  // dynamic slice scheduling, longest slices first (sorder): each warp takes
+  // the next slice from a global counter, so the kernel has no long tail
+  for (;;) {
+    unsigned int i = 0;
+    if (lane == 0) i = atomicAdd(&sched[0], 1u);
+    i = __shfl_sync(0xffffffffu, i, 0);
+    if (i >= nslices) break;
+    const long long s = sorder ? (long long)sorder[i] : (long long)i;
     const bool tr = sflag != nullptr && sflag[s];
     const Tin* __restrict__ x = tr ? xT : xrow;
     const int m = tr ? grid - 1 : -1, sh = tr ? gshift : 0;
@@ -460,6 +466,25 @@ sell_spmv_d16_kernel(long long rows, long long nslices, const long long* __restr
     }
     if (row >= 0 && row < rows) y[row] = acc;
   }
+  // the last warp out resets the scheduler for the next launch
+  if (lane == 0) {
+    __threadfence();
+    const unsigned int done = atomicAdd(&sched[1], 1u);
+    if (done == gridDim.x * (blockDim.x >> 5) - 1) {
+      sched[0] = 0;
+      sched[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
+// slice sizes (for the longest-first order)
+__global__ void sell_slice_size_kernel(long long nslices, const long long* __restrict__ sptr,
+                                       unsigned int* __restrict__ size, int* __restrict__ idx) {
+  const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nslices) return;
+  size[s] = (unsigned int)((sptr[s + 1] - sptr[s]) >> 7);
+  idx[s] = (int)s;
 }
 
 // slot permutation grouping an image's pixels into 8-wide x 4-tall tiles
