@@ -11,6 +11,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -82,32 +83,53 @@ int guarded(F&& f) {
 size_t dsize(int dt) { return dt == HS_F64 ? 8 : (dt == HS_F32 ? 4 : 2); }
 long long round_up(long long a, long long b) { return (a + b - 1) / b * b; }
 
+// Stream-ordered allocations on the context stream of each device, from a
+// memory pool that keeps freed blocks (repeated solves reuse the 7.5 GB of
+// bases instead of paying cudaMalloc/cudaFree and page unmapping each time).
+static cudaStream_t g_dev_stream[64] = {};
+
+static cudaStream_t alloc_stream() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return (d >= 0 && d < 64) ? g_dev_stream[d] : nullptr;
+}
+
 // device buffer with RAII
 struct DBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  cudaStream_t st = nullptr;
   DBuf() = default;
   explicit DBuf(size_t b, bool zero = true) { alloc(b, zero); }
   void alloc(size_t b, bool zero = true) {
     release();
     bytes = b;
     if (b) {
-      CK(cudaMalloc(&p, b));
-      if (zero) CK(cudaMemset(p, 0, b));
+      st = alloc_stream();
+      if (st) {
+        CK(cudaMallocAsync(&p, b, st));
+        if (zero) CK(cudaMemsetAsync(p, 0, b, st));
+      } else {
+        CK(cudaMalloc(&p, b));
+        if (zero) CK(cudaMemset(p, 0, b));
+      }
     }
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (st) cudaFreeAsync(p, st);
+      else cudaFree(p);
+    }
     p = nullptr;
     bytes = 0;
   }
   ~DBuf() { release(); }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes), st(o.st) { o.p = nullptr; o.bytes = 0; }
   DBuf& operator=(DBuf&& o) noexcept {
     release();
-    p = o.p; bytes = o.bytes; o.p = nullptr; o.bytes = 0;
+    p = o.p; bytes = o.bytes; st = o.st; o.p = nullptr; o.bytes = 0;
     return *this;
   }
   template <class T> T* as() const { return reinterpret_cast<T*>(p); }
@@ -595,6 +617,12 @@ struct Solver {
 
   void run(const double* b_h, const double* x0_h, const double* xt_h, hs_result* res) {
     cudaStream_t s = ctx->stream;
+    const bool timing = getenv("HS_TIMING") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+      return std::chrono::duration<double, std::milli>(b - a).count();
+    };
+    const auto t_start = now();
     const bool square = cfg.square != 0;
     const int K = cfg.maxiter;
     const long long m = op->m, n = op->n;
@@ -630,6 +658,8 @@ struct Solver {
     st = stb.as<LoopState>();
     LoopState hst;
 
+    if (timing) CK(cudaStreamSynchronize(s));
+    const auto t_alloc = now();
     CK(cudaMemcpyAsync(bd.p, b_h, m * sizeof(double), cudaMemcpyHostToDevice, s));
     if (x0_h) {
       x0d.alloc(n * sizeof(double), false);
@@ -753,6 +783,8 @@ struct Solver {
       sk0++;
     }
 
+    if (timing) CK(cudaStreamSynchronize(s));
+    const auto t_init = now();
     // ---- the loop (solvers.py:468-538)
     std::vector<cudaEvent_t> ev(K + 1);
     for (auto& e : ev) CK(cudaEventCreate(&e));
@@ -865,6 +897,7 @@ struct Solver {
     res->termination = bd_at ? HS_TERM_BREAKDOWN : HS_TERM_MAXITER;
     res->bd_side = bd_at ? hst.bd_side : -1;
 
+    const auto t_loop = now();
     // ---- final iterate(s): x_kend, and x_{kend-1} when the fused pass skipped it
     auto xpass = [&](int kx, double* xout, double* relslot) {
       const int g = grid_for(n, 256, SMS * 8);
@@ -971,6 +1004,11 @@ struct Solver {
     res->Db = Db;
     res->ldn = ldn;
     res->ldm = ldm;
+    if (timing) {
+      const auto t_end = now();
+      fprintf(stderr, "[hs_solve] alloc %.1f ms, init %.1f ms, loop %.1f ms (device %.1f), finalize %.1f ms\n",
+              ms(t_start, t_alloc), ms(t_alloc, t_init), ms(t_init, t_loop), res->loop_ms, ms(t_loop, t_end));
+    }
   }
 
 };
@@ -996,6 +1034,14 @@ int hs_ctx_create(int device, hs_ctx** out) {
     auto* c = new hs_ctx();
     c->device = device;
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    if (device < 64 && !g_dev_stream[device]) {
+      // keep freed blocks in the device pool (no release back to the driver)
+      cudaMemPool_t pool;
+      CK(cudaDeviceGetDefaultMemPool(&pool, device));
+      unsigned long long thr = ~0ULL;
+      CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+      g_dev_stream[device] = c->stream;
+    }
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     *out = c;
   });
@@ -1010,6 +1056,7 @@ int hs_ctx_destroy(hs_ctx* ctx) {
       cudaEventDestroy(p.b);
     }
     for (auto e : ctx->free_events) cudaEventDestroy(e);
+    if (ctx->device < 64 && g_dev_stream[ctx->device] == ctx->stream) g_dev_stream[ctx->device] = nullptr;
     cudaStreamDestroy(ctx->stream);
     delete ctx;
   });
