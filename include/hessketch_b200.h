@@ -88,6 +88,14 @@ int hs_ctx_synchronize(hs_ctx* ctx);
 /* multi-GPU: NCCL communicator over `nranks` processes (one per GPU) */
 int hs_comm_get_unique_id(void* out_128_bytes);
 int hs_comm_init(hs_ctx* ctx, int nranks, int rank, const void* unique_id_128_bytes);
+int hs_comm_info(const hs_ctx* ctx, int32_t* nranks, int32_t* rank);
+/* test hook: build operators / run solves through the sharded path with one rank */
+int hs_ctx_force_sharding(hs_ctx* ctx, int on);
+/* after hs_comm_init with nranks > 1, hs_op_tomo_create builds only this
+   rank's rows of A (rays) and of A^T (image rows); hs_solve then runs the
+   row-sharded loop and returns the full x on every rank */
+int hs_op_shard_info(const hs_op* op, int64_t* m_off, int64_t* m_loc, int64_t* m_blk, int64_t* n_off,
+                     int64_t* n_loc, int64_t* n_blk);
 
 /* operators: m x n, value dtype HS_F64/HS_F32 (values are uploaded once) */
 int hs_op_dense_create(hs_ctx* ctx, int64_t m, int64_t n, const void* M_rowmajor, int vdtype, hs_op** out);

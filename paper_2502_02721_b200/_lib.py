@@ -57,6 +57,9 @@ _SIGNATURES = [
     ("hs_ctx_kernel_names", c_i32, [c_vp, ctypes.c_char_p, c_i64]),
     ("hs_comm_get_unique_id", c_i32, [c_vp]),
     ("hs_comm_init", c_i32, [c_vp, ctypes.c_int, ctypes.c_int, c_vp]),
+    ("hs_comm_info", c_i32, [c_vp, P_i32, P_i32]),
+    ("hs_ctx_force_sharding", c_i32, [c_vp, ctypes.c_int]),
+    ("hs_op_shard_info", c_i32, [c_vp, P_i64, P_i64, P_i64, P_i64, P_i64, P_i64]),
     ("hs_op_dense_create", c_i32, [c_vp, c_i64, c_i64, c_vp, ctypes.c_int, ctypes.POINTER(c_vp)]),
     ("hs_op_csr_create", c_i32, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.POINTER(c_vp)]),
     ("hs_op_psf_create", c_i32, [c_vp, c_i64, c_i64, c_i32, c_i32, c_vp, ctypes.c_int, ctypes.POINTER(c_vp)]),

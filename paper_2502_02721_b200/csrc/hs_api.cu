@@ -27,6 +27,7 @@
 #include "hs_loop.cuh"
 #include "hs_ops.cuh"
 #include "hs_qr.cuh"
+#include "hs_shard.cuh"
 #include "hs_sketch.cuh"
 
 using namespace hs;
@@ -109,6 +110,8 @@ struct DBuf {
       if (st) {
         CK(cudaMallocAsync(&p, b, st));
         if (zero) CK(cudaMemsetAsync(p, 0, b, st));
+        // buffers are also touched by synchronous copies on the legacy stream
+        CK(cudaStreamSynchronize(st));
       } else {
         CK(cudaMalloc(&p, b));
         if (zero) CK(cudaMemset(p, 0, b));
@@ -158,6 +161,8 @@ struct hs_ctx {
   cudaStream_t stream = nullptr;
   int num_sms = 148;
   int nranks = 1, rank = 0;
+  void* comm = nullptr;  // ncclComm_t when nranks > 1 (hs_dist.inc)
+  bool force_shard = false;  // run the sharded operator/loop even with one rank (tests)
   bool profiling = false;
   std::map<std::string, KStat> stats;
   // pending event pairs for profiled launches
@@ -272,10 +277,12 @@ static void csr_to_sell(hs_ctx* ctx, const Csr& A, Sell& S, int tile_grid = 0) {
   S.cols = A.cols;
   S.nnz = A.nnz;
   if (tile_grid > 0) {
-    const long long tiles = (long long)((tile_grid + 7) / 8) * ((tile_grid + 3) / 4);
+    const long long rows_img = (A.rows + tile_grid - 1) / tile_grid;  // image rows in this block
+    const long long tiles = (long long)((tile_grid + 7) / 8) * ((rows_img + 3) / 4);
     S.nslices = tiles;
     S.rperm.alloc(S.nslots() * sizeof(int), false);
-    tile_perm_kernel<<<grid_for(S.nslots(), 256, 1 << 30), 256, 0, s>>>(tile_grid, S.nslots(), S.rperm.as<int>());
+    tile_perm_block_kernel<<<grid_for(S.nslots(), 256, 1 << 30), 256, 0, s>>>(
+        tile_grid, (int)((A.rows + tile_grid - 1) / tile_grid), S.nslots(), S.rperm.as<int>());
     CKL();
   } else {
     S.nslices = (A.rows + 31) / 32;
@@ -328,6 +335,10 @@ struct hs_op {
   Csr A, At;
   Sell As, Ats;
   bool csr_kept = true;
+  // row sharding (multi-GPU): A rows [m_off, m_off+m_loc), A^T rows [n_off, n_off+n_loc),
+  // padded block sizes m_blk / n_blk (the all-gathered vectors are P*blk long)
+  bool sharded = false;
+  long long m_off = 0, m_loc = 0, m_blk = 0, n_off = 0, n_loc = 0, n_blk = 0;
   // tomography: per-slice transposed-layout flags of As and the scratch copy of x
   int img_grid = 0;
   DBuf sflag;
@@ -581,6 +592,9 @@ struct hs_result {
   std::shared_ptr<DBuf> Lb, Db;
   long long ldn = 0, ldm = 0;
   hs_ctx* ctx = nullptr;
+  // sharded solves keep only this rank's rows of the bases
+  bool sharded = false;
+  long long n_loc = 0, m_loc = 0;
 };
 
 // ---------------------------------------------------------------------------
@@ -1064,22 +1078,8 @@ int hs_ctx_destroy(hs_ctx* ctx) {
 
 int hs_ctx_synchronize(hs_ctx* ctx) { return guarded([&] { CK(cudaStreamSynchronize(ctx->stream)); }); }
 
-int hs_comm_get_unique_id(void* out) {
-  return guarded([&] {
-    (void)out;
-    fail(HS_ERR_NOTIMPL, "multi-GPU communicator not built in this version");
-  });
-}
-
-int hs_comm_init(hs_ctx* ctx, int nranks, int rank, const void* uid) {
-  return guarded([&] {
-    (void)ctx;
-    (void)uid;
-    if (nranks == 1 && rank == 0) return;
-    fail(HS_ERR_NOTIMPL, "multi-GPU communicator not built in this version");
-  });
-}
-
 }  // extern "C"
+
+#include "hs_dist.inc"
 
 #include "hs_abi.inc"

@@ -1,0 +1,89 @@
+"""Multi-GPU plumbing: one process per GPU, NCCL communicator inside the C
+library, torch.distributed only to ship the NCCL unique id.
+
+    import torch.distributed as dist
+    dist.init_process_group("nccl")           # torchrun, MASTER_ADDR=127.0.0.1
+    from paper_2502_02721_b200 import dist as hsd
+    hsd.init_comm()                            # library communicator on this rank's GPU
+    op = TomographyOperator(2048, 720, 2897)   # builds this rank's shard only
+    res = slslu(op, b, cfg, x_true, sketch=S)  # row-sharded loop; full x on every rank
+
+Partition (``shard_plan``, mirrored by hs_dist.inc:build_tomo_sharded): rank r
+owns rays [r*m_blk, r*m_blk + m_loc) -- rows of A and entries of the
+data-side vectors -- and image rows [r*rows_pr, ...) i.e. pixels
+[r*n_blk, r*n_blk + n_loc) -- rows of A^T and entries of the solution-side
+vectors.  Blocks are padded to equal sizes so all-gathers produce the global
+vectors in index order.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+from . import _lib
+
+__all__ = ["ShardPlan", "shard_plan", "init_comm", "comm_info"]
+
+
+def _round_up(a, b):
+    return (a + b - 1) // b * b
+
+
+@dataclass(frozen=True)
+class ShardPlan:
+    m_off: int
+    m_loc: int
+    m_blk: int
+    n_off: int
+    n_loc: int
+    n_blk: int
+
+
+def shard_plan(grid, n_angles, n_bins, nranks, rank):
+    """Row blocks of rank ``rank`` for a grid^2-pixel, n_angles*n_bins-ray
+    operator (same arithmetic as the C library)."""
+    m, n = n_angles * n_bins, grid * grid
+    m_blk = _round_up(-(-m // nranks), 64)
+    m_off = rank * m_blk
+    m_loc = max(0, min(m_blk, m - m_off))
+    rows_pr = _round_up(-(-grid // nranks), 8)
+    n_blk = rows_pr * grid
+    n_off = rank * n_blk
+    n_loc = max(0, min(n_blk, n - n_off))
+    return ShardPlan(m_off, m_loc, m_blk, n_off, n_loc, n_blk)
+
+
+def init_comm(ctx=None):
+    """Create the library's NCCL communicator over the torch.distributed
+    world (rank 0 draws the unique id, torch broadcasts it).  Returns
+    (world_size, rank)."""
+    import torch.distributed as dist
+
+    ctx = ctx or _lib.context()
+    lib = _lib.load()
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
+        _lib.check(lib.hs_comm_init(ctx.handle, 1, 0, None))
+        return 1, 0
+    ws, rank = dist.get_world_size(), dist.get_rank()
+    uid = ctypes.create_string_buffer(128)
+    if rank == 0:
+        _lib.check(lib.hs_comm_get_unique_id(uid))
+    box = [bytes(uid.raw)]
+    dist.broadcast_object_list(box, src=0)
+    raw = ctypes.create_string_buffer(box[0], 128)
+    _lib.check(lib.hs_comm_init(ctx.handle, ws, rank, raw))
+    return ws, rank
+
+
+def comm_info(ctx=None):
+    ctx = ctx or _lib.context()
+    n, r = _lib.c_i32(), _lib.c_i32()
+    _lib.check(_lib.load().hs_comm_info(ctx.handle, ctypes.byref(n), ctypes.byref(r)))
+    return n.value, r.value
+
+
+def force_sharding(on=True, ctx=None):
+    """Test hook: route operators / solves through the sharded path with one rank."""
+    ctx = ctx or _lib.context()
+    _lib.check(_lib.load().hs_ctx_force_sharding(ctx.handle, 1 if on else 0))

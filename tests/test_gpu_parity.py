@@ -412,3 +412,37 @@ def test_relations_at_scale(hs):
     lhs = K @ L[:, :k]
     assert np.linalg.norm(lhs - D @ H) <= 1e-4 * np.linalg.norm(lhs)
     assert all(r.dots == 0 for r in res.trace.records)
+
+
+@pytest.mark.parametrize("lam,basis", [(0.0, "float32"), (1e-3, "float32"), (0.0, "bfloat16")])
+def test_sharded_path_single_rank(hs, lam, basis):
+    """The row-sharded operator build and loop (hs_dist.inc) forced on one rank
+    reproduce the single-GPU path bit for bit."""
+    from paper_2502_02721_b200 import dist as hsd
+    from paper_2502_02721_b200.problems import add_noise, random_ellipses
+
+    grid, angles, bins, K = 48, 30, 69, 30
+    x = random_ellipses(grid, 10, 0).ravel()
+    cfg = hs.SolverConfig(maxiter=K, lam=lam, dtype="float32", basis_dtype=basis, sketch_kind="gaussian")
+    op1 = hs.TomographyOperator(grid, angles, bins, dtype=np.float32)
+    b, _ = add_noise(op1.matvec(x), 0.01, 1)
+    S = hs.SparseSignSketch(4 * K, op1.rows, seed=2, zeta=8)
+    sk = hs.SketchOperator(4 * K, op1.rows, 2, S)
+    r1 = hs.slslu(op1, b, cfg, x_true=x, sketch=sk)
+    hsd.force_sharding(True)
+    try:
+        op2 = hs.TomographyOperator(grid, angles, bins, dtype=np.float32)
+        np.testing.assert_array_equal(op2.matvec(x), op1.matvec(x))
+        r2 = hs.slslu(op2, b, cfg, x_true=x, sketch=sk)
+    finally:
+        hsd.force_sharding(False)
+    f1, f2 = r1.factorization, r2.factorization
+    np.testing.assert_array_equal(f2.t[:K + 1], f1.t[:K + 1])
+    np.testing.assert_array_equal(f2.g[:K + 1], f1.g[:K + 1])
+    np.testing.assert_array_equal(f2.H_matrix(), f1.H_matrix())
+    np.testing.assert_array_equal(f2.W_matrix(), f1.W_matrix())
+    np.testing.assert_array_equal(f2.L_matrix(), f1.L_matrix())
+    np.testing.assert_array_equal(r2.x, r1.x)
+    assert r2.trace.column("sres_norm") == r1.trace.column("sres_norm")
+    assert r2.trace.column("rel_err") == r1.trace.column("rel_err")
+    assert r2.trace.column("sketches") == r1.trace.column("sketches")
