@@ -159,6 +159,7 @@ struct KStat {
 struct hs_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t aux = nullptr;  // second stream: sketches + projected solve overlap the basis passes
   int num_sms = 148;
   int nranks = 1, rank = 0;
   void* comm = nullptr;  // ncclComm_t when nranks > 1 (hs_dist.inc)
@@ -207,16 +208,18 @@ struct Prof {
   const char* name;
   double bytes;
   cudaEvent_t a = nullptr;
-  Prof(hs_ctx* c_, const char* n, double b) : c(c_), name(n), bytes(b) {
+  cudaStream_t st;
+  Prof(hs_ctx* c_, const char* n, double b, cudaStream_t s_ = nullptr)
+      : c(c_), name(n), bytes(b), st(s_ ? s_ : c_->stream) {
     if (c->profiling) {
       a = c->get_event();
-      CK(cudaEventRecord(a, c->stream));
+      CK(cudaEventRecord(a, st));
     }
   }
   ~Prof() noexcept(false) {
     if (c->profiling) {
       cudaEvent_t b = c->get_event();
-      CK(cudaEventRecord(b, c->stream));
+      CK(cudaEventRecord(b, st));
       c->pending.push_back({name, a, b, bytes});
       if (c->pending.size() > 4096) c->harvest();
     }
@@ -540,15 +543,15 @@ struct hs_sketch {
   uint2 key() const { return make_uint2((unsigned)seed, (unsigned)(seed >> 32)); }
 
   template <class Tin>
-  void apply_t(const void* v, double* z) const {
-    cudaStream_t s = ctx->stream;
+  void apply_t(const void* v, double* z, cudaStream_t st) const {
+    cudaStream_t s = st ? st : ctx->stream;
     const Tin* vi = reinterpret_cast<const Tin*>(v);
     if (kind == HS_SKETCH_DENSE) {
-      Prof p(ctx, "sketch_dense", (double)ell * m * 8);
+      Prof p(ctx, "sketch_dense", (double)ell * m * 8, s);
       sketch_dense_kernel<double, Tin><<<(int)ell, 256, 0, s>>>((int)ell, m, S.as<double>(), m, vi, z);
       CKL();
     } else if (kind == HS_SKETCH_GAUSSIAN) {
-      Prof p(ctx, "sketch_gauss", (double)m * sizeof(Tin));
+      Prof p(ctx, "sketch_gauss", (double)m * sizeof(Tin), s);
       const int nq = (int)((ell + 3) / 4);
       dim3 grid(ntiles, (nq + 63) / 64);
       sketch_gauss_partial_kernel<Tin><<<grid, 256, 0, s>>>((int)ell, m, 0, tile_cols, key(), vi, part.as<double>());
@@ -557,21 +560,21 @@ struct hs_sketch {
                                                                             1.0 / std::sqrt((double)ell), z);
       CKL();
     } else if (kind == 3) {
-      Prof p(ctx, "sketch_csr", 0.0);
+      Prof p(ctx, "sketch_csr", 0.0, s);
       sketch_csr_kernel<Tin><<<(int)ell, 256, 0, s>>>((int)ell, rowptr.as<long long>(), scol.as<int>(),
                                                       cval.as<double>(), vi, z);
       CKL();
     } else {
-      Prof p(ctx, "sketch_sparse", (double)m * zeta * 4 + (double)m * sizeof(Tin));
+      Prof p(ctx, "sketch_sparse", (double)m * zeta * 4 + (double)m * sizeof(Tin), s);
       sketch_sparse_kernel<Tin><<<(int)ell, 256, 0, s>>>((int)ell, rowptr.as<long long>(), scol.as<int>(), 0, m, vi,
                                                          1.0 / std::sqrt((double)zeta), z);
       CKL();
     }
   }
-  void apply(const void* v, int vdt, double* z) const {
-    if (vdt == HS_F64) apply_t<double>(v, z);
-    else if (vdt == HS_F32) apply_t<float>(v, z);
-    else apply_t<__nv_bfloat16>(v, z);
+  void apply(const void* v, int vdt, double* z, cudaStream_t st = nullptr) const {
+    if (vdt == HS_F64) apply_t<double>(v, z, st);
+    else if (vdt == HS_F32) apply_t<float>(v, z, st);
+    else apply_t<__nv_bfloat16>(v, z, st);
   }
 };
 
@@ -814,7 +817,7 @@ struct Solver {
     const bool rec_x = cfg.record_x && xt_h;
     const size_t elim_smem_base = 16;
     auto elim = [&](T* vec, long long len, long long ldv, const B* basis, int k, int side, int iter, int kx,
-                    const double* yx, double* relerr_slot) {
+                    const double* yx, double* relerr_slot, T* vout) {
       const long long nvec = (len + VEC - 1) / VEC;
       const int g = grid_for(nvec, 256, CAND_CAP);
       const size_t smem = ((k * sizeof(T) + 15) / 16) * 16 + (size_t)kx * sizeof(double) + elim_smem_base;
@@ -827,9 +830,28 @@ struct Solver {
       kern<<<g, 256, smem, s>>>(
           len, 0, basis, square || side == 1 ? ldn : ldm, nullptr, k, cvec.as<T>(), vec, kx, yx, nullptr,
           x0_h ? x0d.as<double>() : nullptr, kx ? xtd.as<double>() : nullptr, xpart.as<double>(), relerr_slot,
-          candp.as<Cand>(), st, side, iter, 1);
+          candp.as<Cand>(), st, side, iter, 1, vout);
       CKL();
     };
+
+    // Two streams (column sketching): the sketch of u = A l_k and the projected
+    // solve of iteration k run on ctx->aux while the main stream does the
+    // basis work; u is not overwritten by the elimination (it writes u2), the
+    // next A-apply waits for the sketch to have read u, and the fused iterate
+    // of iteration k+1 waits for y^{(k)}.
+    const bool ovl = !sb;
+    cudaStream_t s2 = ovl ? ctx->aux : s;
+    DBuf u2(ovl ? ldm * sizeof(T) : 0);
+    T* uel = ovl ? u2.as<T>() : u.as<T>();  // elimination output on the side that is sketched
+    cudaEvent_t ev_u, ev_sk, ev_qr, ev_l;
+    CK(cudaEventCreateWithFlags(&ev_u, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_sk, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_qr, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_l, cudaEventDisableTiming));
+    if (ovl) {  // the aux stream starts after the init work (sr0, F col 0) on the main stream
+      CK(cudaEventRecord(ev_l, s));
+      CK(cudaStreamWaitEvent(s2, ev_l, 0));
+    }
 
     // host-side breakdown polling (pinned flag copied at the end of each iteration)
     int* hflag = nullptr;
@@ -851,38 +873,49 @@ struct Solver {
       const int kx = (rec_x && k >= 2) ? k - 1 : 0;
       const double* yprev = kx ? Yh.as<double>() + (long long)(k - 2) * K : nullptr;
       double* relslot = kx ? rel2.as<double>() + (k - 2) : nullptr;
+      // u is free once the previous iteration's sketch has read it
+      if (ovl && k > 1) CK(cudaStreamWaitEvent(s, ev_sk, 0));
+      op->apply(Lcol(k - 1), bdt, u.p, wdt, false);
+      if (ovl) {
+        CK(cudaEventRecord(ev_u, s));
+        CK(cudaStreamWaitEvent(s2, ev_u, 0));
+        S2->apply(u.p, wdt, Zb.as<double>() + (long long)(k - 1) * ell, s2);
+        CK(cudaEventRecord(ev_sk, s2));
+      }
+      // the fused iterate x_{k-1} needs y^{(k-1)} from the aux stream
+      auto wait_y = [&] {
+        if (ovl && kx) CK(cudaStreamWaitEvent(s, ev_qr, 0));
+      };
       if (!square) {
-        op->apply(Lcol(k - 1), bdt, u.p, wdt, false);
-        if (!sb) S2->apply(u.p, wdt, Zb.as<double>() + (long long)(k - 1) * ell);
         fsub(u.as<T>(), tpos.as<long long>(), PD.as<T>(), ldp, k, k, 0, cvec.as<T>(), Hcol(k - 1));
-        elim(u.as<T>(), m, ldm, D, k, 0, k, 0, nullptr, nullptr);
+        elim(u.as<T>(), m, ldm, D, k, 0, k, 0, nullptr, nullptr, uel);
         pivot_commit_kernel<T, B><<<1, 256, 0, s>>>(k, m, Hcol(k - 1), tpos.as<long long>(), PD.as<T>(), ldp, D, ldm,
                                                     0, m, st, 0, k, pv.as<T>());
         CKL();
-        normalize_kernel<T, B><<<grid_for(ldm, 256, NORM_G), 256, 0, s>>>(m, ldm, u.as<T>(), pv.as<T>(), Dcol(k), st, 0, k);
+        normalize_kernel<T, B><<<grid_for(ldm, 256, NORM_G), 256, 0, s>>>(m, ldm, uel, pv.as<T>(), Dcol(k), st, 0, k);
         CKL();
         if (sb) S2->apply(Dcol(k), bdt, Gb.as<double>() + (long long)k * ell);
         op->apply(Dcol(k), bdt, q.p, wdt, true);
         fsub(q.as<T>(), gpos.as<long long>(), PL.as<T>(), ldp, k, k, 1, cvec.as<T>(), Wcol(k));
-        elim(q.as<T>(), n, ldn, L, k, 1, k, kx, yprev, relslot);
+        wait_y();
+        elim(q.as<T>(), n, ldn, L, k, 1, k, kx, yprev, relslot, q.as<T>());
         pivot_commit_kernel<T, B><<<1, 256, 0, s>>>(k, n, Wcol(k), gpos.as<long long>(), PL.as<T>(), ldp, L, ldn, 0,
                                                     n, st, 1, k, pv.as<T>() + 1);
         CKL();
         normalize_kernel<T, B><<<grid_for(ldn, 256, NORM_G), 256, 0, s>>>(n, ldn, q.as<T>(), pv.as<T>() + 1, Lcol(k), st, 1, k);
         CKL();
       } else {
-        op->apply(Lcol(k - 1), bdt, u.p, wdt, false);
-        if (!sb) S2->apply(u.p, wdt, Zb.as<double>() + (long long)(k - 1) * ell);
+        if (!ovl && !sb) S2->apply(u.p, wdt, Zb.as<double>() + (long long)(k - 1) * ell);
         fsub(u.as<T>(), tpos.as<long long>(), PL.as<T>(), ldp, k, k, 0, cvec.as<T>(), Hcol(k - 1));
-        elim(u.as<T>(), n, ldn, L, k, 0, k, kx, yprev, relslot);
+        wait_y();
+        elim(u.as<T>(), n, ldn, L, k, 0, k, kx, yprev, relslot, uel);
         pivot_commit_kernel<T, B><<<1, 256, 0, s>>>(k, n, Hcol(k - 1), tpos.as<long long>(), PL.as<T>(), ldp, L, ldn,
                                                     0, n, st, 0, k, pv.as<T>());
         CKL();
-        normalize_kernel<T, B><<<grid_for(ldn, 256, NORM_G), 256, 0, s>>>(n, ldn, u.as<T>(), pv.as<T>(), Lcol(k), st, 0, k);
+        normalize_kernel<T, B><<<grid_for(ldn, 256, NORM_G), 256, 0, s>>>(n, ldn, uel, pv.as<T>(), Lcol(k), st, 0, k);
         CKL();
         if (sb) S2->apply(Lcol(k), bdt, Gb.as<double>() + (long long)k * ell);
       }
-      if (lamon) S1->apply(Lcol(k), bdt, Fb.as<double>() + (long long)k * ell);
       if (sb) {
         // M column k-1 = G[:, :k+1] @ H[:k+1, k-1]  (zero columns/entries past a breakdown)
         gemv_small_kernel<<<grid_for(ell, 128, 1 << 30), 128, 0, s>>>((int)ell, k + 1, Gb.as<double>(), Hcol(k - 1),
@@ -892,16 +925,33 @@ struct Solver {
       qa.zcol = Zb.as<double>() + (long long)(k - 1) * ell;
       qa.fcol = lamon ? Fb.as<double>() + (long long)(k - 1) * ell : nullptr;
       {
-        Prof p(ctx, "qr_step", 0.0);
+        Prof p(ctx, "qr_step", 0.0, s2);
         int kk = k, it = k;
         void* args[] = {&qa, &kk, &it};
-        CK(cudaLaunchCooperativeKernel((void*)qr_step_kernel, dim3(NB), dim3(256), args, qr_smem, s));
+        CK(cudaLaunchCooperativeKernel((void*)qr_step_kernel, dim3(NB), dim3(256), args, qr_smem, s2));
         ++g_launches;
+      }
+      if (ovl) CK(cudaEventRecord(ev_qr, s2));
+      if (lamon) {
+        // F column k = S1 l_{k+1} (used by the projected solve of iteration k+1)
+        if (ovl) {
+          CK(cudaEventRecord(ev_l, s));
+          CK(cudaStreamWaitEvent(s2, ev_l, 0));
+        }
+        S1->apply(Lcol(k), bdt, Fb.as<double>() + (long long)k * ell, s2);
       }
       CK(cudaEventRecord(ev[k], s));
       CK(cudaMemcpyAsync(hflag + k, &st->bd_iter, sizeof(int), cudaMemcpyDeviceToHost, s));
       CK(cudaEventRecord(flag_ev[k], s));
     }
+    // join the aux stream (last sketch / projected solve) before timing and readback
+    cudaEvent_t ev_end;
+    CK(cudaEventCreate(&ev_end));
+    if (ovl) {
+      CK(cudaEventRecord(ev_sk, s2));
+      CK(cudaStreamWaitEvent(s, ev_sk, 0));
+    }
+    CK(cudaEventRecord(ev_end, s));
     CK(cudaStreamSynchronize(s));
     CK(cudaMemcpy(&hst, st, sizeof(LoopState), cudaMemcpyDeviceToHost));
     bd_at = hst.bd_iter;
@@ -927,16 +977,17 @@ struct Solver {
     if (rec_x && kend >= 2 && data_bd) xpass(kend - 1, nullptr, rel2.as<double>() + (kend - 2));
     CK(cudaStreamSynchronize(s));
     float lms = 0;
-    CK(cudaEventElapsedTime(&lms, ev[0], ev[kend]));
+    CK(cudaEventElapsedTime(&lms, ev[0], kend == k_last ? ev_end : ev[kend]));
     res->loop_ms = lms;
     res->wall_ms.resize(kend);
     for (int k = 1; k <= kend; ++k) {
       float w = 0;
-      CK(cudaEventElapsedTime(&w, ev[k - 1], ev[k]));
+      CK(cudaEventElapsedTime(&w, ev[k - 1], (k == kend && kend == k_last) ? ev_end : ev[k]));
       res->wall_ms[k - 1] = w;
     }
     for (auto& e : ev) cudaEventDestroy(e);
     for (auto& e : flag_ev) cudaEventDestroy(e);
+    for (auto e : {ev_u, ev_sk, ev_qr, ev_l, ev_end}) cudaEventDestroy(e);
     cudaFreeHost(hflag);
 
     // ---- copy back
@@ -1048,6 +1099,7 @@ int hs_ctx_create(int device, hs_ctx** out) {
     auto* c = new hs_ctx();
     c->device = device;
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
     if (device < 64 && !g_dev_stream[device]) {
       // keep freed blocks in the device pool (no release back to the driver)
       cudaMemPool_t pool;
@@ -1071,6 +1123,8 @@ int hs_ctx_destroy(hs_ctx* ctx) {
     }
     for (auto e : ctx->free_events) cudaEventDestroy(e);
     if (ctx->device < 64 && g_dev_stream[ctx->device] == ctx->stream) g_dev_stream[ctx->device] = nullptr;
+    cudaStreamSynchronize(ctx->aux);
+    cudaStreamDestroy(ctx->aux);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
   });

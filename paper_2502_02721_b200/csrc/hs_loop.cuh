@@ -156,12 +156,12 @@ template <> struct VecLoad<__nv_bfloat16, 8> {
 template <class T, class B, int VEC, bool XF>
 __global__ void __launch_bounds__(256)
 elim_pass_kernel(long long n, long long idx_offset, const B* __restrict__ basis, long long ld,
-                 const int* __restrict__ kptr, int kfixed, const T* __restrict__ cvec, T* __restrict__ u,
+                 const int* __restrict__ kptr, int kfixed, const T* __restrict__ cvec, const T* u,
                  int kx, const double* __restrict__ yx, double* __restrict__ xout,
                  const double* __restrict__ x0, const double* __restrict__ xt,
                  double* __restrict__ xpart, double* __restrict__ relerr_out,
                  Cand* __restrict__ cand_part, LoopState* __restrict__ st, int side, int iter,
-                 int write_u) {
+                 int write_u, T* uo) {
   if (st->bd_iter != 0 && st->bd_iter < iter) return;
   if (side == 1 && st->bd_iter == iter) return;  // data side broke down this iteration
   extern __shared__ unsigned char smem_raw[];
@@ -211,7 +211,7 @@ elim_pass_kernel(long long n, long long idx_offset, const B* __restrict__ basis,
     for (int q = 0; q < VEC; ++q) {
       const long long e = e0 + q;
       if (e < n) {
-        if (write_u) u[e] = acc[q];
+        if (write_u) uo[e] = acc[q];  // uo may alias u (read above, same element)
         const double mg = (double)absval(acc[q]);
         if (better(mg, idx_offset + e, best.mag, best.idx)) best = Cand{mg, (double)acc[q], idx_offset + e};
         if (XF && kx > 0) {
