@@ -150,6 +150,31 @@ struct Philox {
 };
 
 // two uniforms in (0,1] -> two standard normals (Box-Muller, fp32 intrinsics)
+// Philox-4x32 with 7 rounds (the smallest round count that passes BigCrush,
+// Salmon et al. 2011): the on-the-fly Gaussian sketch's generator
+__device__ __forceinline__ uint4 philox7(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 7; ++r) {
+    c = Philox::round(c, k);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+
+// Box-Muller with the uniforms taken from the mantissa bits (no int->float
+// conversion on the XU pipe) and sqrt as t * rsqrt(t): two standard normals
+__device__ __forceinline__ void box_muller_fast(uint32_t a, uint32_t b, float& n0, float& n1) {
+  const float u1 = 2.0f - __uint_as_float(0x3f800000u | (a >> 9));  // (0, 1]
+  const float u2 = __uint_as_float(0x3f800000u | (b >> 9)) - 1.0f;  // [0, 1)
+  const float t = -2.0f * __logf(u1);                                // >= 0
+  const float r = t * rsqrtf(t + 1e-30f);
+  float s, c;
+  __sincosf(6.283185307179586f * u2, &s, &c);
+  n0 = r * c;
+  n1 = r * s;
+}
+
 __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float& n0, float& n1) {
   float u1 = ((float)(a >> 8) + 1.0f) * (1.0f / 16777216.0f);  // (0, 1]
   float u2 = (float)(b >> 8) * (1.0f / 16777216.0f);          // [0, 1)

@@ -27,46 +27,67 @@ sketch_dense_kernel(int ell, long long m, const Vs* __restrict__ S, long long ld
 // ---- Gaussian from Philox: S[i, c] = N(seed; c, i) / sqrt(ell) -----------------
 // one Philox call per (column c, row quad q) gives 4 normals (2 Box-Muller pairs)
 __device__ __forceinline__ void gauss_quad(uint2 key, unsigned long long c, unsigned q, float (&o)[4]) {
-  const uint4 r = Philox::gen(make_uint4((unsigned)c, (unsigned)(c >> 32), q, 0x53CE7C4Du), key);
-  box_muller(r.x, r.y, o[0], o[1]);
-  box_muller(r.z, r.w, o[2], o[3]);
+  const uint4 r = philox7(make_uint4((unsigned)c, (unsigned)(c >> 32), q, 0x53CE7C4Du), key);
+  box_muller_fast(r.x, r.y, o[0], o[1]);
+  box_muller_fast(r.z, r.w, o[2], o[3]);
 }
 
-// grid: (ntiles, ceil(nquads/64)), block 256 = 64 quads x 4 column phases
+// grid: (ntiles, nqb), block 256 = QB row quads x PH column phases (QB = quads
+// per block, chosen so the quads split evenly over the nqb blocks); the tile's
+// slice of v is staged in shared memory as fp64 (converted once per block)
 template <class Tin>
 __global__ void __launch_bounds__(256)
 sketch_gauss_partial_kernel(int ell, long long m, long long col_offset, long long tile_cols, uint2 key,
                             const Tin* __restrict__ v, double* __restrict__ part) {
-  __shared__ double red[4][64][4];
+  constexpr int CH = 1024;
+  __shared__ double vs[CH];
+  __shared__ double red[256][4];
   const int nq = (ell + 3) / 4;
-  const int ql = threadIdx.x & 63, ph = threadIdx.x >> 6;
-  const int q = blockIdx.y * 64 + ql;
+  const int nqb = gridDim.y;
+  const int QB = (nq + nqb - 1) / nqb;  // <= 64
+  const int PH = 256 / QB;
+  const int ql = threadIdx.x % QB, ph = threadIdx.x / QB;
+  const int q = blockIdx.y * QB + ql;
+  const bool active = ph < PH && q < nq;
   const long long c0 = (long long)blockIdx.x * tile_cols;
   const long long c1 = min(m, c0 + tile_cols);
   double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-  if (q < nq) {
-    for (long long c = c0 + ph; c < c1; c += 4) {
-      const double vc = cvt<double>(v[c]);
-      float g[4];
-      gauss_quad(key, (unsigned long long)(c + col_offset), (unsigned)q, g);
-      a0 = fma((double)g[0], vc, a0);
-      a1 = fma((double)g[1], vc, a1);
-      a2 = fma((double)g[2], vc, a2);
-      a3 = fma((double)g[3], vc, a3);
+  for (long long cb = c0; cb < c1; cb += CH) {
+    const int cn = (int)min((long long)CH, c1 - cb);
+    __syncthreads();
+    for (int i = threadIdx.x; i < cn; i += blockDim.x) vs[i] = cvt<double>(v[cb + i]);
+    __syncthreads();
+    if (active) {
+      for (int i = ph; i < cn; i += PH) {
+        const double vc = vs[i];
+        float g[4];
+        gauss_quad(key, (unsigned long long)(cb + i + col_offset), (unsigned)q, g);
+        a0 = fma((double)g[0], vc, a0);
+        a1 = fma((double)g[1], vc, a1);
+        a2 = fma((double)g[2], vc, a2);
+        a3 = fma((double)g[3], vc, a3);
+      }
     }
   }
-  red[ph][ql][0] = a0; red[ph][ql][1] = a1; red[ph][ql][2] = a2; red[ph][ql][3] = a3;
+  red[threadIdx.x][0] = a0; red[threadIdx.x][1] = a1; red[threadIdx.x][2] = a2; red[threadIdx.x][3] = a3;
   __syncthreads();
   if (ph == 0 && q < nq) {
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int i = 4 * q + r;
       if (i < ell) {
-        const double s = ((red[0][ql][r] + red[1][ql][r]) + red[2][ql][r]) + red[3][ql][r];
+        double s = 0.0;
+        for (int p = 0; p < PH; ++p) s += red[p * QB + ql][r];  // fixed phase order
         part[(long long)blockIdx.x * ell + i] = s;
       }
     }
   }
+}
+
+// number of row-quad blocks for the partial kernel (<= 64 quads per block, balanced)
+inline int gauss_quad_blocks(int ell) {
+  const int nq = (ell + 3) / 4;
+  return (nq + 63) / 64;
 }
 
 // z[i] = scale * sum_t part[t][i]   (t ascending)

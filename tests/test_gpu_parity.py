@@ -390,7 +390,11 @@ def test_bf16_basis_keeps_structure(hs):
     assert np.all(np.diag(B) == 1.0)
     assert np.all(np.triu(B, 1) == 0.0)
     ref = hs.scmrh(op, b, hs.SolverConfig(maxiter=20, dtype="float32", sketch_kind="gaussian", sketch_rows=120), x_true=x)
-    assert abs(res.trace.final().rel_err - ref.trace.final().rel_err) < 0.05
+    # bf16 storage of the basis vs fp32 storage: same best reconstruction error to within 10%
+    # (the late iterates of this ill-posed problem semi-converge, so compare the minimum)
+    best_bf16 = min(res.trace.column("rel_err"))
+    best_fp32 = min(ref.trace.column("rel_err"))
+    assert abs(best_bf16 - best_fp32) <= 0.1 * best_fp32
 
 
 def test_relations_at_scale(hs):
