@@ -440,6 +440,13 @@ out:
 
 int co_max_threads(void) { return omp_get_max_threads(); }
 
+/* y = A x in float32, sequential no-FMA row sums (scipy csr_matvec order): the
+   full-size operator checker for the device SpMV */
+void co_spmv_f32_export(int64_t rows, const int64_t* rp, const int32_t* ci, const float* cv, const float* x, float* y,
+                        int nthreads) {
+  spmv_f32(rows, rp, ci, cv, x, y, nthreads);
+}
+
 /* y = A x with float values and float64 x / y (input generation: b = A x_true) */
 void co_spmv_f32_f64(int64_t rows, const int64_t* rp, const int32_t* ci, const float* cv, const double* x, double* y,
                      int nthreads) {

@@ -38,6 +38,7 @@ def lib():
         _lib.co_slslu_f32.restype = ctypes.c_int
         _lib.co_max_threads.restype = ctypes.c_int
         _lib.co_spmv_f32_f64.argtypes = [i64, vp, vp, vp, vp, vp, i32]
+        _lib.co_spmv_f32_export.argtypes = [i64, vp, vp, vp, vp, vp, i32]
     return _lib
 
 
