@@ -42,6 +42,17 @@ METRIC = "sketched-LSLU iterations/sec at 2048^2 tomography; achieved HBM GB/s"
 UNIT = "iterations/s"
 
 
+def _traffic(args):
+    """DRAM bytes per SpMV launch from the committed ncu capture (config 4 only)."""
+    if args.config != 4 or args.scale:
+        return None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1", "traffic.json")) as fh:
+            return float(json.load(fh)["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -221,13 +232,15 @@ def run_ours(args, ws, rank, local):
                 "d2h_bytes_per_step": int(w.x_true.nbytes + 8 * 12 * K)},
         "roofline": {
             "bound": "hbm",
-            "kernel": "csr_seq_spmv (A and A^T)",
+            "kernel": "sell_spmv_d16_kernel (A and A^T; 6 B/nonzero encoding, see DESIGN.md)",
+            "achieved_csr8_equiv": (round(achieved * (8.0 * inf["nnz"]) / (sp_bytes / sp_launch), 1)
+                                    if achieved and inf.get("nnz") and ws == 1 else None),
             "achieved": round(achieved, 1) if achieved else None,
             "peak": peak,
             "unit": "GB/s",
             "frac": round(achieved / peak, 4) if achieved else None,
             "peak_source": peak_kind,
-            "traffic": None,
+            "traffic": _traffic(args),
             "share_of_step": round(sp_ms / (sum(loop_ms)), 4) if loop_ms else None,
         },
         "gpu_launches": int(launches),
