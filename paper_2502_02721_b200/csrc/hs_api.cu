@@ -138,6 +138,12 @@ struct DBuf {
   template <class T> T* as() const { return reinterpret_cast<T*>(p); }
 };
 
+// experiment switches (tools/ab_spmv.py): set and not "0"/empty
+bool env_flag(const char* name) {
+  const char* e = getenv(name);
+  return e && *e && !(e[0] == '0' && e[1] == 0);
+}
+
 int grid_for(long long work, int block, int cap) {
   long long g = (work + block - 1) / block;
   if (g < 1) g = 1;
@@ -202,6 +208,34 @@ struct hs_ctx {
   }
 };
 
+// Experiment (HS_L2PERSIST=1): keep the gathered vector resident in L2 while
+// the matrix streams past it (stream access-policy window, persisting hits).
+struct L2Window {
+  cudaStream_t s = nullptr;
+  L2Window(cudaStream_t st, const void* p, size_t bytes) {
+    const bool on = env_flag("HS_L2PERSIST");
+    if (!on || p == nullptr) return;
+    static bool limit_set = false;
+    if (!limit_set) {
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)64 << 20);
+      limit_set = true;
+    }
+    cudaStreamAttrValue a = {};
+    a.accessPolicyWindow.base_ptr = const_cast<void*>(p);
+    a.accessPolicyWindow.num_bytes = bytes;
+    a.accessPolicyWindow.hitRatio = 1.0f;
+    a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    if (cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &a) == cudaSuccess) s = st;
+  }
+  ~L2Window() {
+    if (!s) return;
+    cudaStreamAttrValue a = {};
+    a.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &a);
+  }
+};
+
 // scoped profiling bracket around one launch
 struct Prof {
   hs_ctx* c;
@@ -245,7 +279,12 @@ struct Sell {
   long long nslots() const { return nslices * 32; }
   bool d16 = false;   // columns stored as int16 deltas (rbase + dcol) instead of col
   DBuf rbase, dcol;
-  double index_bytes() const { return d16 ? 2.0 : 4.0; }
+  bool c8 = false;    // columns stored as 8-bit transition codes (hs_ops.cuh: C8Geom)
+  C8Geom c8g{0, 0};
+  DBuf code, xoff, exc;
+  long long n_exc = 0;
+  double index_bytes() const { return c8 ? 1.0 : d16 ? 2.0 : 4.0; }
+  double slot_bytes() const { return c8 ? 12.0 : d16 ? 8.0 : 4.0; }  // rlen (+ rbase) (+ escape offset) per slot
 };
 
 // Switch a SELL copy to 16-bit column deltas when every in-row step fits.
@@ -269,6 +308,48 @@ static bool sell_try_delta16(hs_ctx* ctx, Sell& S) {
   CK(cudaStreamSynchronize(s));
   S.col.release();
   S.d16 = true;
+  return true;
+}
+
+// Switch a SELL copy of a tomography operator to 8-bit transition codes
+// (hs_ops.cuh: C8Geom).  `span` = number of distinct r values (image rows /
+// angles), used to bound the gather addresses.  Opt-in (HS_C8=1 for A,
+// HS_AT_C8=1 for A^T): inside the solve loop, where the SM clock sits at the
+// power cap, the 5 B/nonzero stream measured slower than 16-bit deltas
+// (A: 3.94 vs 3.80 ms at 2048^2), though 2% faster in isolation.
+static bool sell_try_code8(hs_ctx* ctx, Sell& S, C8Geom g, long long span, const unsigned char* sflag) {
+  if (S.nslices == 0) return false;
+  if (g.mode == 0 && span * (long long)g.G >= (1LL << 31)) return false;
+  if (g.mode == 1 && ((span + 3) / 4) * 4 * (long long)g.G >= (1LL << 30)) return false;
+  cudaStream_t s = ctx->stream;
+  const long long ns = S.nslots();
+  S.code.alloc(std::max<long long>(S.slots, 4), false);
+  S.rbase.alloc(std::max<long long>(ns, 1) * sizeof(int), false);
+  DBuf cnt((ns + 1) * sizeof(int));
+  S.xoff.alloc((ns + 1) * sizeof(int), false);
+  const int gb = (int)grid_for(S.nslices, 8, 1 << 30);
+  sell_c8_encode_kernel<<<gb, 256, 0, s>>>(S.nslices, S.sptr.as<long long>(), S.rlen.as<int>(), S.col.as<int>(), sflag,
+                                           g, 0, S.code.as<unsigned char>(), S.rbase.as<int>(), cnt.as<int>(), nullptr,
+                                           nullptr);
+  CKL();
+  {
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt.as<int>(), S.xoff.as<int>(), ns + 1, s));
+    DBuf t(tmp, false);
+    CK(cub::DeviceScan::ExclusiveSum(t.p, tmp, cnt.as<int>(), S.xoff.as<int>(), ns + 1, s));
+  }
+  int nx = 0;
+  CK(cudaMemcpyAsync(&nx, S.xoff.as<int>() + ns, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  S.n_exc = nx;
+  S.exc.alloc(std::max(nx, 1) * sizeof(int), false);
+  sell_c8_encode_kernel<<<gb, 256, 0, s>>>(S.nslices, S.sptr.as<long long>(), S.rlen.as<int>(), S.col.as<int>(), sflag,
+                                           g, 1, nullptr, nullptr, nullptr, S.xoff.as<int>(), S.exc.as<int>());
+  CKL();
+  CK(cudaStreamSynchronize(s));
+  S.col.release();
+  S.c8 = true;
+  S.c8g = g;
   return true;
 }
 
@@ -346,6 +427,10 @@ struct hs_op {
   int img_grid = 0;
   DBuf sflag;
   mutable DBuf xT;
+  // tomography: A^T gathers from a blocked copy of the sinogram (hs_ops.cuh: SinoBlk)
+  SinoBlk sblk{0, 0, 0, 0};
+  long long n_angles = 0;
+  mutable DBuf yB;
   // psf
   int H = 0, W = 0, kh = 0, kw = 0;
   DBuf K;
@@ -360,9 +445,18 @@ struct hs_op {
       const int grid = grid_for(M.nslices, 8, ctx->num_sms * 16);
       // algorithmic bytes of the stored encoding: values + column indices (4 B, or 2 B deltas)
       // + row lengths (+ row bases) + slice pointers + x once + y
-      const double bytes = (double)M.nnz * (sizeof(V) + M.index_bytes()) + (double)M.rows * (M.d16 ? 8 : 4) +
-                           (double)M.nslices * 8 + (double)M.cols * sizeof(Tin) + (double)M.rows * sizeof(T);
+      const double bytes = (double)M.nnz * (sizeof(V) + M.index_bytes()) + (double)M.rows * M.slot_bytes() +
+                           (double)M.n_exc * 4 + (double)M.nslices * 8 + (double)M.cols * sizeof(Tin) +
+                           (double)M.rows * sizeof(T);
       const bool tflag = !transpose && sflag.p != nullptr;
+      if (transpose && sblk.n_bins > 0) {
+        Prof p(ctx, "y_block", 2.0 * (double)m * sizeof(Tin));
+        const size_t need = (size_t)sblk.size(n_angles) * sizeof(Tin);
+        if (yB.bytes < need) yB.alloc(need, false);
+        sino_block_kernel<Tin><<<grid_for(m, 256, ctx->num_sms * 8), 256, 0, s>>>(m, sblk, xi, yB.as<Tin>());
+        CKL();
+        xi = yB.as<Tin>();
+      }
       if (tflag) {
         // transposed image copy of x for the near-horizontal ray slices
         Prof p(ctx, "x_transpose", 2.0 * (double)n * sizeof(Tin));
@@ -373,14 +467,27 @@ struct hs_op {
         CKL();
       }
       Prof p(ctx, transpose ? "spmv_AT" : "spmv_A", bytes);
-      if (M.d16) {
+      L2Window l2w(s, xi, (size_t)M.cols * sizeof(Tin));
+      if (M.c8) {
+        // 3-deep ring, 6 blocks of 8 warps per SM (fp32); fp64 values / work fit 3 blocks
+        constexpr int MINB = (sizeof(T) == 4 && sizeof(V) == 4) ? 6 : 3;
+        auto kern = M.c8g.mode == 0 ? sell_spmv_c8_kernel<V, Tin, T, 0, 3, MINB> : sell_spmv_c8_kernel<V, Tin, T, 1, 3, MINB>;
+        const int smem = C8Lane<V, 3>::smem_bytes(256);
+        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        kern<<<grid, 256, smem, s>>>(M.rows, M.nslices, M.sptr.as<long long>(), M.rlen.as<int>(), M.rbase.as<int>(),
+                                  M.code.as<unsigned char>(), M.xoff.as<int>(), M.exc.as<int>(), M.val.as<V>(), xi,
+                                  tflag ? xT.as<Tin>() : nullptr, tflag ? sflag.as<unsigned char>() : nullptr, M.c8g.G,
+                                  M.rperm.as<int>(), transpose ? nullptr : M.sorder.as<int>(),
+                                  M.sched.as<unsigned int>(), yo);
+      } else if (M.d16) {
         int gshift = -1;
         if (img_grid > 0 && (img_grid & (img_grid - 1)) == 0) gshift = __builtin_ctz((unsigned)img_grid);
         auto kern = (gshift >= 0 || !tflag) ? sell_spmv_d16_kernel<V, Tin, T, true> : sell_spmv_d16_kernel<V, Tin, T, false>;
         kern<<<grid, 256, 0, s>>>(M.rows, M.nslices, M.sptr.as<long long>(), M.rlen.as<int>(), M.rbase.as<int>(),
                                   M.dcol.as<short>(), M.val.as<V>(), xi, tflag ? xT.as<Tin>() : nullptr,
                                   tflag ? sflag.as<unsigned char>() : nullptr, img_grid, gshift >= 0 ? gshift : 0,
-                                  M.rperm.as<int>(), transpose ? nullptr : M.sorder.as<int>(),
+                                  M.rperm.as<int>(),
+                                  transpose ? nullptr : M.sorder.as<int>(),
                                   M.sched.as<unsigned int>(), yo);
       } else {
         sell_spmv_kernel<V, Tin, T><<<grid, 256, 0, s>>>(M.rows, M.nslices, M.sptr.as<long long>(), M.rlen.as<int>(),

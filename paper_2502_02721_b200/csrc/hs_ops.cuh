@@ -183,6 +183,10 @@ template <> struct Chunk4<float> {
     float4 t = __ldcs(reinterpret_cast<const float4*>(p));
     return Chunk4{{t.x, t.y, t.z, t.w}};
   }
+  static __device__ __forceinline__ Chunk4 lds(const void* p) {
+    const float4 t = *reinterpret_cast<const float4*>(p);
+    return Chunk4{{t.x, t.y, t.z, t.w}};
+  }
 };
 template <> struct Chunk4<double> {
   double v[4];
@@ -191,8 +195,19 @@ template <> struct Chunk4<double> {
     double2 b = __ldcs(reinterpret_cast<const double2*>(p) + 1);
     return Chunk4{{a.x, a.y, b.x, b.y}};
   }
+  static __device__ __forceinline__ Chunk4 lds(const void* p) {
+    const double2 a = reinterpret_cast<const double2*>(p)[0], b = reinterpret_cast<const double2*>(p)[1];
+    return Chunk4{{a.x, a.y, b.x, b.y}};
+  }
 };
 
+// ---- shared-memory address / L2 policy helpers ----
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ unsigned long long l2_evict_first_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 template <class T, class Tin> __device__ __forceinline__ T gather_x(const Tin* __restrict__ x, int c) {
   return cvt<T>(__ldg(x + c));
 }
@@ -270,6 +285,32 @@ __global__ void __launch_bounds__(256) image_transpose_kernel(int grid, const Ti
     const int gx = bx + r, gy = by + tx;  // output row = original column
     if (gx < grid && gy < grid) xT[(long long)gx * grid + gy] = tile[tx][r];
   }
+}
+
+// ---- blocked sinogram layout for the A^T gathers --------------------------------
+// A^T's columns are rays r = angle*n_bins + bin.  The 32 lanes of an 8x4 pixel
+// tile drift apart in angle as they step through their rows, so in ray order
+// one gather touches ~16 lines.  In the blocked layout a 128-byte line holds an
+// (ab angles x bb bins) block, and the same gather touches ~9 lines
+// (tools/ab_spmv.py; the sum order is unchanged, only the gather address).
+struct SinoBlk {
+  int n_bins, ab, bb, nbb;  // nbb = bin blocks per angle block
+  __host__ __device__ long long map(long long c) const {
+    const long long a = c / n_bins, b = c - a * n_bins;
+    return ((a / ab) * nbb + b / bb) * (ab * bb) + (a % ab) * bb + (b % bb);
+  }
+  __host__ __device__ long long size(long long n_angles) const { return ((n_angles + ab - 1) / ab) * nbb * ab * bb; }
+};
+
+__global__ void sino_block_cols_kernel(long long n, SinoBlk B, int* __restrict__ col) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    col[i] = (int)B.map(col[i]);
+}
+
+template <class Tin>
+__global__ void sino_block_kernel(long long m, SinoBlk B, const Tin* __restrict__ y, Tin* __restrict__ yb) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x)
+    yb[B.map(i)] = y[i];
 }
 
 // Choose, per slice, the image layout in which the 32 lanes' gathers touch
@@ -467,6 +508,260 @@ sell_spmv_d16_kernel(long long rows, long long nslices, const long long* __restr
     if (row >= 0 && row < rows) y[row] = acc;
   }
   // the last warp out resets the scheduler for the next launch
+  if (lane == 0) {
+    __threadfence();
+    const unsigned int done = atomicAdd(&sched[1], 1u);
+    if (done == gridDim.x * (blockDim.x >> 5) - 1) {
+      sched[0] = 0;
+      sched[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
+// ---- 8-bit transition codes (tomography operators) ---------------------------------
+// The columns of a tomography row are points (r, c) of a 2D index space that
+// a ray (or, for A^T, a pixel's sequence of rays) walks through in small steps:
+//   A   : (image row, image column); consecutive entries move right along an
+//         image row or step to the next image row (+1 row, small column move);
+//   A^T : (angle, detector bin); consecutive entries move to the next bin or
+//         to the next angle (+1 angle, small bin move).
+// Each entry after the first is one byte (dr << 7) | (dc & 0x7f), dr in {0,1},
+// dc in [-64, 63]; anything else (and the reserved byte 0xC0) is an escape
+// whose absolute gather address sits in a per-lane exception list.  Stored
+// bytes per nonzero: 4 (fp32 value) + 1, against 4 + 2 for 16-bit deltas.
+// The decoder keeps the gather ADDRESS, so the per-slice layout choice of A
+// (image / transposed image) and the 4-angle interleave of the sinogram for
+// A^T cost nothing extra:
+//   mode 0: address r*G + c, or c*G + r on transposed slices (G = grid)
+//   mode 1: address (r>>2)*4*G + 4*c + (r&3)   (G = n_bins; r&3 kept in bits 30-31 of escapes)
+struct C8Geom {
+  int mode, G;
+  __device__ __forceinline__ int addr(int r, int c, bool tr) const {
+    if (mode == 0) return tr ? c * G + r : r * G + c;
+    return ((r >> 2) * 4 * G + c * 4 + (r & 3)) | ((r & 3) << 30);
+  }
+};
+constexpr unsigned int C8_ESC = 0xC0u;
+
+// pass 0: codes, first addresses and per-slot escape counts; pass 1: escape lists
+__global__ void sell_c8_encode_kernel(long long nslices, const long long* __restrict__ sptr,
+                                      const int* __restrict__ rlen, const int* __restrict__ col,
+                                      const unsigned char* __restrict__ sflag, C8Geom g, int pass,
+                                      unsigned char* __restrict__ code, int* __restrict__ rbase,
+                                      int* __restrict__ xcnt, const int* __restrict__ xoff, int* __restrict__ exc) {
+  const long long s = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (s >= nslices) return;
+  const int lane = threadIdx.x & 31;
+  const long long slot = s * 32 + lane;
+  const int len = rlen[slot];
+  const long long base = sptr[s];
+  const int ne = (int)((sptr[s + 1] - base) >> 7) * 4;
+  const bool tr = g.mode == 0 && sflag != nullptr && sflag[s];
+  int pr = 0, pc = 0, nx = 0, xp = pass ? xoff[slot] : 0;
+  for (int e = 0; e < ne; ++e) {
+    const long long sl = base + (long long)(e >> 2) * 128 + lane * 4 + (e & 3);
+    unsigned int b = 0;
+    if (e < len) {
+      const int cc = col[sl];
+      const int r = cc / g.G, c = cc - r * g.G;
+      if (e == 0) {
+        if (pass == 0) rbase[slot] = g.addr(r, c, tr);
+      } else {
+        const int dr = r - pr, dc = c - pc;
+        if ((dr == 0 || dr == 1) && dc >= -64 && dc <= 63 && !(dr == 1 && dc == -64)) {
+          b = ((unsigned)dr << 7) | ((unsigned)dc & 0x7fu);
+        } else {
+          b = C8_ESC;
+          if (pass == 1) exc[xp] = g.addr(r, c, tr);
+          ++xp;
+          ++nx;
+        }
+      }
+      pr = r;
+      pc = c;
+    }
+    if (pass == 0) code[sl] = (unsigned char)b;
+  }
+  if (pass == 0) {
+    xcnt[slot] = nx;
+    if (len == 0) rbase[slot] = 0;
+  }
+}
+
+template <int MODE>
+struct C8Dec {
+  int addr, ra, SR, SC;
+  __device__ __forceinline__ void init(int a0, bool tr, int G) {
+    if (MODE == 0) {
+      addr = a0;
+      SR = tr ? 1 : G;
+      SC = tr ? G : 1;
+      ra = 0;
+    } else {
+      addr = a0 & 0x3fffffff;
+      ra = (int)((unsigned)a0 >> 30);
+      SR = 4 * G - 3;  // address step when the angle enters the next 4-angle group
+      SC = 4;
+    }
+  }
+  // apply byte j of w (not an escape)
+  __device__ __forceinline__ void step(unsigned int w, int j) {
+    const int dc = ((int)(w << (25 - 8 * j))) >> 25;
+    const int dr = (int)((w >> (8 * j + 7)) & 1u);
+    if (MODE == 0) {
+      addr += dc * SC + (dr ? SR : 0);
+    } else {
+      ra += dr;
+      addr += dc * 4 + (dr ? ((ra & 3) ? 1 : SR) : 0);
+    }
+  }
+  __device__ __forceinline__ void esc(int e) {
+    if (MODE == 0) {
+      addr = e;
+    } else {
+      addr = e & 0x3fffffff;
+      ra = (int)((unsigned)e >> 30);
+    }
+  }
+  // decode a chunk into four addresses; lanes with pending escapes check each byte
+  __device__ __forceinline__ void chunk(unsigned int w, int& xp, int xe, const int* __restrict__ exc, int (&a)[4]) {
+    if (xp < xe) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (((w >> (8 * j)) & 0xffu) == C8_ESC) esc(__ldg(exc + xp++));
+        else step(w, j);
+        a[j] = addr;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        step(w, j);
+        a[j] = addr;
+      }
+    }
+  }
+};
+
+// SpMV over the 8-bit coded SELL layout.  The (value, code) stream is moved
+// by LDGSTS (cp.async): every lane copies its own 16 B of values and 4 B of
+// codes per chunk straight into a per-thread NS-deep shared-memory ring, so
+// NS-1 chunks per lane are in flight while chunk q is consumed without
+// holding registers (a register double buffer holds one and measured 13%
+// slower; a TMA bulk-copy ring per warp, 2x the instructions).  Each lane
+// reads back only what it copied: no cross-lane hand-off, independent trip
+// counts.  Per chunk: decode 4 codes, 4 gathers, 4 ordered multiply-adds.
+__device__ __forceinline__ void cpasync16(unsigned dst, const void* src, unsigned long long pol) {
+#ifdef HS_CPASYNC_HINT
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(pol) : "memory");
+#else
+  (void)pol;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+#endif
+}
+__device__ __forceinline__ void cpasync4(unsigned dst, const void* src, unsigned long long pol) {
+#ifdef HS_CPASYNC_HINT
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "l"(pol) : "memory");
+#else
+  (void)pol;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+#endif
+}
+__device__ __forceinline__ void cpasync_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpasync_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <class V, int NS>
+struct C8Lane {
+  static constexpr int VB = 4 * (int)sizeof(V);  // value bytes per lane per chunk
+  static constexpr int smem_bytes(int threads) { return NS * threads * (VB + 4); }
+};
+
+template <class V, class Tin, class T, int MODE, int NS, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+sell_spmv_c8_kernel(long long rows, long long nslices, const long long* __restrict__ sptr,
+                     const int* __restrict__ rlen, const int* __restrict__ rbase, const unsigned char* __restrict__ code,
+                     const int* __restrict__ xoff, const int* __restrict__ exc, const V* __restrict__ val,
+                     const Tin* __restrict__ xrow, const Tin* __restrict__ xT, const unsigned char* __restrict__ sflag,
+                     int G, const int* __restrict__ rperm, const int* __restrict__ sorder,
+                     unsigned int* __restrict__ sched, T* __restrict__ y) {
+  using L = C8Lane<V, NS>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  // ring slot st of this thread: values at vs + st*VSTR, code word at cs + st*CSTR
+  const unsigned vs = smem_u32(smem_raw) + threadIdx.x * L::VB;
+  const unsigned cs = smem_u32(smem_raw) + NS * blockDim.x * L::VB + threadIdx.x * 4;
+  const unsigned VSTR = blockDim.x * L::VB, CSTR = blockDim.x * 4;
+  const unsigned long long pol = l2_evict_first_policy();
+  for (;;) {
+    unsigned int i = 0;
+    if (lane == 0) i = atomicAdd(&sched[0], 1u);
+    i = __shfl_sync(0xffffffffu, i, 0);
+    if (i >= nslices) break;
+    const long long s = sorder ? (long long)sorder[i] : (long long)i;
+    const long long base = sptr[s];
+    const long long slot = s * 32 + lane;
+    const int len = rlen[slot];
+    const int nq = (len + 3) >> 2, nfull = len >> 2;
+    const V* vp = val + base + lane * 4;
+    const unsigned char* cp = code + base + lane * 4;
+    // prologue: chunks 0 .. NS-2
+#pragma unroll
+    for (int k = 0; k < NS - 1; ++k) {
+      if (k < nq) {
+        cpasync16(vs + k * VSTR, vp + (long long)k * 128, pol);
+        if (sizeof(V) == 8) cpasync16(vs + k * VSTR + 16, vp + (long long)k * 128 + 2, pol);
+        cpasync4(cs + k * CSTR, cp + (long long)k * 128, pol);
+      }
+      cpasync_commit();
+    }
+    const bool tr = MODE == 0 && sflag != nullptr && sflag[s];
+    const Tin* __restrict__ x = tr ? xT : xrow;
+    const long long row = rperm ? (long long)rperm[slot] : slot;
+    C8Dec<MODE> dec;
+    dec.init(rbase[slot], tr, G);
+    int xp = xoff[slot];
+    const int xe = xoff[slot + 1];
+    T acc = T(0);
+    int st = 0;
+    for (int q = 0; q < nq; ++q) {
+      {  // refill the slot consumed last iteration with chunk q + NS - 1
+        const int k = q + NS - 1;
+        const int sk = st == 0 ? NS - 1 : st - 1;
+        if (k < nq) {
+          cpasync16(vs + sk * VSTR, vp + (long long)k * 128, pol);
+          if (sizeof(V) == 8) cpasync16(vs + sk * VSTR + 16, vp + (long long)k * 128 + 2, pol);
+          cpasync4(cs + sk * CSTR, cp + (long long)k * 128, pol);
+        }
+        cpasync_commit();
+      }
+      cpasync_wait<NS - 1>();
+      const Chunk4<V> v = Chunk4<V>::lds(smem_raw + threadIdx.x * L::VB + st * VSTR);
+      const unsigned w = *reinterpret_cast<const unsigned*>(smem_raw + NS * VSTR + threadIdx.x * 4 + st * CSTR);
+      st = st + 1 == NS ? 0 : st + 1;
+      int a[4];
+      dec.chunk(w, xp, xe, exc, a);
+      if (q < nfull) {
+        const T x0 = gather_x<T>(x, a[0]);
+        const T x1 = gather_x<T>(x, a[1]);
+        const T x2 = gather_x<T>(x, a[2]);
+        const T x3 = gather_x<T>(x, a[3]);
+        acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[0]), x0));
+        acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[1]), x1));
+        acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[2]), x2));
+        acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[3]), x3));
+      } else {
+        const int rem = len & 3;
+        acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[0]), gather_x<T>(x, a[0])));
+        if (rem > 1) acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[1]), gather_x<T>(x, a[1])));
+        if (rem > 2) acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[2]), gather_x<T>(x, a[2])));
+      }
+    }
+    cpasync_wait<0>();
+    if (row >= 0 && row < rows) y[row] = acc;
+  }
   if (lane == 0) {
     __threadfence();
     const unsigned int done = atomicAdd(&sched[1], 1u);

@@ -2,6 +2,8 @@
 reference's golden fixtures.  Bit-exact for operator row sums, pivots, bases
 and H/W; tolerances stated per test for the projected-solve quantities."""
 
+import os
+
 import numpy as np
 import pytest
 import scipy.sparse
@@ -126,6 +128,44 @@ def test_tomography_builder_general_bins(hs, grid, angles, bins):
     np.testing.assert_array_equal(got.data, want.data)
     op32 = hs.TomographyOperator(grid, angles, bins, dtype=np.float32)
     np.testing.assert_array_equal(op32.export().data, want.data.astype(np.float32).astype(np.float64))
+
+
+@pytest.mark.parametrize("grid,angles,bins", [(128, 720, 181), (200, 360, 283)])
+@pytest.mark.parametrize(
+    "env",
+    [{}, {"HS_C8": "1"}, {"HS_AT_C8": "1"}, {"HS_SINO_BLK": "0"}, {"HS_C8": "1", "HS_SINO_BLK": "2x16"}],
+    ids=["default", "a_c8", "at_c8", "ray_order", "a_c8_blk2x16"],
+)
+def test_tomography_encodings_bitwise(hs, monkeypatch, grid, angles, bins, env):
+    """Every device encoding of the tomography operator (8-bit transition codes
+    with escape lists, 16-bit deltas, blocked / interleaved / ray-order
+    sinogram gathers, transposed-image slices) applies exactly the reference
+    CSR: fp32 work bitwise vs the C port of csr_matvec, fp64 work bitwise vs
+    scipy on the same fp32 values.  0.25-0.5 degree angles make runs longer
+    than 64 pixels, i.e. escape entries in the 8-bit code."""
+    import scipy.sparse as sp
+
+    from oracle import cpu_baseline as cb
+
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    A, At, m, n = cb.host_tomography(grid, angles, bins, os.cpu_count())
+    op = hs.TomographyOperator(grid, angles, bins, dtype=np.float32)
+    rng = np.random.default_rng(grid)
+    x = rng.standard_normal(n).astype(np.float32)
+    y = rng.standard_normal(m).astype(np.float32)
+
+    def host32(M, v):
+        out = np.empty(len(M[0]) - 1, dtype=np.float32)
+        cb.lib().co_spmv_f32_export(len(M[0]) - 1, cb._p(M[0]), cb._p(M[1]), cb._p(M[2]), cb._p(v), cb._p(out), 1)
+        return out
+
+    np.testing.assert_array_equal(op.matvec(x, np.float32), host32(A, x))
+    np.testing.assert_array_equal(op.rmatvec(y, np.float32), host32(At, y))
+    S = sp.csr_matrix((A[2].astype(np.float64), A[1], A[0]), shape=(m, n))
+    St = sp.csr_matrix((At[2].astype(np.float64), At[1], At[0]), shape=(n, m))
+    np.testing.assert_array_equal(op.matvec(x.astype(np.float64), np.float64), S @ x.astype(np.float64))
+    np.testing.assert_array_equal(op.rmatvec(y.astype(np.float64), np.float64), St @ y.astype(np.float64))
 
 
 # ---------------------------------------------------------------------------
