@@ -14,8 +14,9 @@
  *   hs_op_apply             LinearOperator.apply / apply_transpose   linops.py:107-125
  *   hs_sketch_create        SketchOperator / make_gaussian_sketch    sketch.py:29-53
  *   hs_sketch_apply         sketch_apply                             sketch.py:56-65
- *   hs_solve                _hessenberg_solve (sketched branch)      solvers.py:410-539
+ *   hs_solve                _hessenberg_solve                        solvers.py:410-539
  *                           via scmrh / slslu / *_tikhonov           solvers.py:562-605
+ *                           and cmrh / lslu (unsketched)             solvers.py:542-559
  *   hs_result_*             SolveResult / SolverTrace / state        solvers.py:119-160,
  *                                                                    hessenberg.py:132-158, 229-272
  *
@@ -68,6 +69,19 @@ typedef struct {
   int32_t basis_dtype;   /* HS_F64 / HS_F32 / HS_BF16 storage of the bases       */
   int32_t record_x;      /* keep x of every iteration for rel_err (needs x_true) */
   double lam;            /* Tikhonov lambda >= 0                                  */
+  int32_t sketched;      /* 1: scmrh / slslu family; 0: unsketched cmrh / lslu
+                            (solvers.py:542-559: min |H y - beta e1|, + lam^2 |y|^2;
+                            S2 / S1 must then be NULL)                            */
+  int32_t pivot_sample;  /* 0: full pivoting; s > 0: PivotStrategy.sampled(s)
+                            (hessenberg.py:93-124)                                */
+  /* pivot_sample > 0: the positions rng.choice(pop, s, replace=False) drawn by
+     the host for each selection, row-major [slot][s]; slot 0 = r0, then
+     square: slot k = step k; rectangular: slot 1 = A^T r0, slots 2k / 2k+1 =
+     step k data / solution side.  Slots whose population (dim - k) is <= s
+     are not read (full scan, no draw), exactly as the reference skips the
+     draw.  Positions index the swap-ordered admissible list t[k:] / g[k:]
+     (hessenberg.py:127-129), which the device maintains.                   */
+  const int64_t* pivot_positions;
 } hs_config;
 
 const char* hs_last_error(void);
@@ -129,7 +143,7 @@ int hs_sketch_export_csr(hs_sketch* sk, int64_t* indptr, int32_t* indices, doubl
 int hs_sketch_destroy(hs_sketch* sk);
 
 /* the solve: b[m], x0[n] or NULL, x_true[n] or NULL (host float64).
-   S1 is required iff cfg->lam > 0. */
+   Sketched: S2 required, S1 required iff cfg->lam > 0.  Unsketched: both NULL. */
 int hs_solve(hs_ctx* ctx, hs_op* op, const hs_config* cfg, hs_sketch* S2, hs_sketch* S1, const double* b,
              const double* x0, const double* x_true, hs_result** out);
 

@@ -163,6 +163,26 @@ def pivot_full(v, admissible):
     return idx, v[idx]
 
 
+def pivot_select(v, admissible, sample_size=0, rng=None):
+    """``pivot_select`` (hessenberg.py:93-115) with the sampled strategy:
+    when ``0 < sample_size < len(admissible)`` the candidates are
+    ``rng.choice(admissible, sample_size, replace=False)``."""
+    admissible = np.asarray(admissible, dtype=np.int64)
+    if admissible.size == 0:
+        raise ValueError("admissible index set is empty")
+    if sample_size and sample_size < admissible.size:
+        admissible = rng.choice(admissible, size=sample_size, replace=False)
+    return pivot_full(v, admissible)
+
+
+def pivot_with_fallback(v, admissible, sample_size=0, rng=None):
+    """hessenberg.py:118-124: a sampled miss (all zero) rescans everything."""
+    idx, val = pivot_select(v, admissible, sample_size, rng)
+    if val == 0.0 and sample_size:
+        idx, val = pivot_full(v, admissible)
+    return idx, val
+
+
 def _swap_to_position(perm, used, idx):
     """hessenberg.py:127-129."""
     pos = used + int(np.nonzero(perm[used:] == idx)[0][0])
@@ -183,6 +203,8 @@ class SquareState:
     breakdown: bool
     r0: np.ndarray
     last_product: np.ndarray = None
+    sample_size: int = 0
+    rng: object = None
 
     def H_matrix(self, rows=None):
         k = len(self.h_cols)
@@ -192,8 +214,8 @@ class SquareState:
         return H if rows is None else H[:rows]
 
 
-def init_square(A, b, x0=None):
-    """hessenberg.py:160-188 (full pivoting)."""
+def init_square(A, b, x0=None, sample_size=0, rng=None):
+    """hessenberg.py:160-188 (full or sampled pivoting)."""
     if not A.is_square:
         raise ValueError("the square Hessenberg process needs a square operator")
     dt = A.dtype
@@ -202,12 +224,14 @@ def init_square(A, b, x0=None):
         raise ValueError(f"b must have length {A.rows}")
     r0 = b.copy() if x0 is None else b - A.apply(np.asarray(x0, dtype=dt))
     t = np.arange(A.rows)
-    idx, beta = pivot_full(r0, t)
+    idx, beta = pivot_with_fallback(r0, t, sample_size, rng)
     if beta == 0.0:
         x = np.zeros(A.cols) if x0 is None else np.asarray(x0, dtype=np.float64).copy()
         raise TrivialSolution("initial residual is zero; starting point is exact", x)
     _swap_to_position(t, 0, idx)
-    return SquareState([r0 / beta], [], t, beta, 0, False, r0)
+    st = SquareState([r0 / beta], [], t, beta, 0, False, r0)
+    st.sample_size, st.rng = sample_size, rng
+    return st
 
 
 def _eliminate(u, basis, perm, k):
@@ -232,7 +256,7 @@ def step_square(state, A, keep_product=True):
         state.last_product = u.copy()
     u, h = _eliminate(u, state.L, state.t, k)
     if k < n:
-        idx, val = pivot_full(u, state.t[k:])
+        idx, val = pivot_with_fallback(u, state.t[k:], state.sample_size, state.rng)
     else:
         val = 0.0
     if val == 0.0:
@@ -266,6 +290,8 @@ class GenState:
     r0: np.ndarray
     last_data_product: np.ndarray = None
     last_solution_product: np.ndarray = None
+    sample_size: int = 0
+    rng: object = None
 
     def H_matrix(self, rows=None):
         k = len(self.h_cols)
@@ -282,8 +308,8 @@ class GenState:
         return W if rows is None else W[:rows]
 
 
-def init_generalized(A, b, x0=None):
-    """hessenberg.py:275-326 (full pivoting)."""
+def init_generalized(A, b, x0=None, sample_size=0, rng=None):
+    """hessenberg.py:275-326 (full or sampled pivoting)."""
     dt = A.dtype
     b = np.asarray(b, dtype=dt)
     if b.shape != (A.rows,):
@@ -291,14 +317,14 @@ def init_generalized(A, b, x0=None):
     r0 = b.copy() if x0 is None else b - A.apply(np.asarray(x0, dtype=dt))
     zero_x = np.zeros(A.cols) if x0 is None else np.asarray(x0, dtype=np.float64).copy()
     t = np.arange(A.rows)
-    idx, beta = pivot_full(r0, t)
+    idx, beta = pivot_with_fallback(r0, t, sample_size, rng)
     if beta == 0.0:
         raise TrivialSolution("initial residual is zero; starting point is exact", zero_x)
     d1 = r0 / beta
     _swap_to_position(t, 0, idx)
     v0 = A.apply_transpose(r0)
     g = np.arange(A.cols)
-    idx2, alpha = pivot_full(v0, g)
+    idx2, alpha = pivot_with_fallback(v0, g, sample_size, rng)
     if alpha == 0.0:
         raise TrivialSolution(
             "transposed residual is zero; the normal equations already hold", zero_x
@@ -309,6 +335,7 @@ def init_generalized(A, b, x0=None):
     st = GenState([d1], [l1], [], [np.array([r[g[0]]], dtype=np.float64)], t, g,
                   beta, alpha, 0, False, r0)
     st.last_solution_product = r.copy()
+    st.sample_size, st.rng = sample_size, rng
     return st
 
 
@@ -323,7 +350,7 @@ def step_generalized(state, A, keep_products=True):
         state.last_data_product = u.copy()
     u, h = _eliminate(u, state.D, state.t, k)
     if k < m:
-        idx, val = pivot_full(u, state.t[k:])
+        idx, val = pivot_with_fallback(u, state.t[k:], state.sample_size, state.rng)
     else:
         val = 0.0
     if val == 0.0:
@@ -343,7 +370,7 @@ def step_generalized(state, A, keep_products=True):
         state.last_solution_product = q.copy()
     q, w = _eliminate(q, state.L, state.g, k)
     if k < n:
-        idx2, val2 = pivot_full(q, state.g[k:])
+        idx2, val2 = pivot_with_fallback(q, state.g[k:], state.sample_size, state.rng)
     else:
         val2 = 0.0
     if val2 == 0.0:
@@ -462,10 +489,14 @@ class Result:
 
 def hessenberg_solve(
     A, b, *, square, maxiter, ell=None, lam=0.0, seed=0, S2=None, S1=None,
-    x0=None, x_true=None, sketch_basis=False,
+    x0=None, x_true=None, sketch_basis=False, sketched=True, pivot_sample=0, pivot_seed=0,
 ):
     """Restates ``_hessenberg_solve`` (solvers.py:410-539) for the sketched
-    solvers ``scmrh`` / ``slslu`` / ``*_tikhonov`` (solvers.py:562-605).
+    solvers ``scmrh`` / ``slslu`` / ``*_tikhonov`` (solvers.py:562-605) and,
+    with ``sketched=False``, the unsketched ``cmrh`` / ``lslu``
+    (solvers.py:542-559: projected problem H_{k+1,k} y ~ beta e1, plus
+    lam^2 |y|^2).  ``pivot_sample`` > 0 selects sampled pivoting
+    (``PivotStrategy.sampled(pivot_sample, pivot_seed)``, hessenberg.py:48-73).
 
     ``S2`` / ``S1``: explicit sketch matrices (anything supporting ``@``).  When
     None they are drawn exactly as the reference draws them
@@ -479,10 +510,13 @@ def hessenberg_solve(
     A = A.fresh()
     c = A.counters
     init = init_square if square else init_generalized
+    rng = np.random.default_rng(pivot_seed) if pivot_sample else None
     try:
-        state = init(A, b, x0=x0)
+        state = init(A, b, x0=x0, sample_size=pivot_sample, rng=rng)
     except TrivialSolution as sig:
         return Result(x=sig.x, records=[], termination="trivial")
+    if not sketched:
+        return _unsketched_loop(A, c, state, square, maxiter, lam, x0, x_true)
 
     if S2 is not None:
         if S2.shape[1] != A.rows:
@@ -562,6 +596,44 @@ def hessenberg_solve(
         Z=np.column_stack(Z_cols) if Z_cols else None,
         F=np.column_stack(F_cols) if F_cols else None, sr0=sr0, loop_seconds=loop_s,
     )
+
+
+def _unsketched_loop(A, c, state, square, maxiter, lam, x0, x_true):
+    """solvers.py:468-539 with ``sketched=False``: M = H_{k+1,k}, rhs = beta e1,
+    N = I_k when lam > 0; no sketch is applied and sres_norm stays None."""
+    records = []
+    termination = "maxiter"
+    x = None
+    x0_64 = None if x0 is None else np.asarray(x0, dtype=np.float64)
+    tic_all = time.perf_counter()
+    for k in range(1, maxiter + 1):
+        tic = time.perf_counter()
+        if square:
+            step_square(state, A, keep_product=False)
+        else:
+            step_generalized(state, A, keep_products=False)
+        Lk = np.column_stack(state.L[:k]).astype(np.float64)
+        M = state.H_matrix()
+        rhs = np.zeros(M.shape[0])
+        rhs[0] = state.beta
+        N = np.eye(k) if lam > 0.0 else None
+        y, fallback = projected_solve(M, rhs, lam, N)
+        x = Lk @ y
+        if x0_64 is not None:
+            x = x0_64 + x
+        rec = dict(iteration=k, proj_obj=objective(M, rhs, y, lam, N), sres_norm=None, rel_err=None,
+                   rank_fallback=fallback)
+        if x_true is not None:
+            xt = np.asarray(x_true, dtype=np.float64)
+            rec["rel_err"] = float(np.linalg.norm(x - xt) / np.linalg.norm(xt))
+        rec["matvecs"], rec["tmatvecs"], rec["dots"], rec["sketches"] = c.snapshot()
+        rec["wall_ms"] = (time.perf_counter() - tic) * 1e3
+        records.append(rec)
+        if state.breakdown:
+            termination = "breakdown"
+            break
+    return Result(x=x, records=records, termination=termination, state=state,
+                  loop_seconds=time.perf_counter() - tic_all)
 
 
 def pivots_of(state):

@@ -37,6 +37,9 @@ from .solvers import (
     SolverConfig,
     SolverTrace,
     TraceRecord,
+    cmrh,
+    lslu,
+    pivot_positions,
     scmrh,
     scmrh_tikhonov,
     slslu,

@@ -40,6 +40,9 @@ class HsConfig(ctypes.Structure):
         ("basis_dtype", ctypes.c_int32),
         ("record_x", ctypes.c_int32),
         ("lam", ctypes.c_double),
+        ("sketched", ctypes.c_int32),
+        ("pivot_sample", ctypes.c_int32),
+        ("pivot_positions", ctypes.c_void_p),
     ]
 
 

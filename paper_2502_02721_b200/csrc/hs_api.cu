@@ -750,7 +750,10 @@ struct Solver {
     const bool square = cfg.square != 0;
     const int K = cfg.maxiter;
     const long long m = op->m, n = op->n;
-    const long long ell = S2->ell;
+    // unsketched cmrh / lslu (solvers.py:542-559): the projected matrix is H
+    // itself ((K+1) rows), rhs beta e1, penalty columns e_j (N = I)
+    const bool skd = cfg.sketched != 0;
+    const long long ell = skd ? S2->ell : (long long)K + 1;
     const bool lamon = cfg.lam > 0.0;
     const bool sb = cfg.sketch_basis != 0;
     const long long ldm = round_up(m, 64), ldn = round_up(n, 64);
@@ -781,6 +784,43 @@ struct Solver {
     DBuf stb(sizeof(LoopState));
     st = stb.as<LoopState>();
     LoopState hst;
+
+    // sampled pivoting (hessenberg.py:93-129): host-drawn positions per
+    // selection slot, device copies of the permutations t / g and inverses
+    const int ps = cfg.pivot_sample;
+    DBuf posd, permT, whereT, permG, whereG;
+    if (ps > 0) {
+      const int nslots = square ? K + 1 : 2 * K + 2;
+      posd.alloc((size_t)nslots * ps * sizeof(long long), false);
+      CK(cudaMemcpy(posd.p, cfg.pivot_positions, (size_t)nslots * ps * sizeof(long long), cudaMemcpyHostToDevice));
+      const long long dt = square ? n : m;
+      for (DBuf* b : {&permT, &whereT}) {
+        b->alloc(dt * sizeof(long long), false);
+        iota_kernel<<<grid_for(dt, 256, 1 << 30), 256, 0, s>>>(b->as<long long>(), (int)dt);
+        CKL();
+      }
+      if (!square) {
+        for (DBuf* b : {&permG, &whereG}) {
+          b->alloc(n * sizeof(long long), false);
+          iota_kernel<<<grid_for(n, 256, 1 << 30), 256, 0, s>>>(b->as<long long>(), (int)n);
+          CKL();
+        }
+      }
+    }
+    // the sampled pick after the full-scan winner is in st (no draw when the
+    // admissible population dim - used is <= the sample size)
+    auto sample = [&](const T* v, long long dim, long long used, int slot, int side, int iter) {
+      if (ps <= 0 || used >= dim || (long long)ps >= dim - used) return;
+      sample_pick_kernel<T><<<1, 256, 0, s>>>(v, (side == 0 ? permT : permG).template as<long long>(), used,
+                                              posd.as<long long>() + (long long)slot * ps, ps, st, side, iter);
+      CKL();
+    };
+    auto swap_perm = [&](int side, long long used) {
+      if (ps <= 0) return;
+      perm_swap_kernel<<<1, 1, 0, s>>>((side == 0 ? permT : permG).template as<long long>(),
+                                       (side == 0 ? whereT : whereG).template as<long long>(), used, st, side);
+      CKL();
+    };
 
     if (timing) CK(cudaStreamSynchronize(s));
     const auto t_alloc = now();
@@ -835,6 +875,7 @@ struct Solver {
       const int g = grid_for(len, 256, SMS * 4);
       argmax_kernel<T><<<g, 256, 0, s>>>(len, 0, v, candp.as<Cand>(), st, side);
       CKL();
+      sample(v, len, 0, side, side, 0);
       CK(cudaMemcpyAsync(&hst, st, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       val = hst.piv_val[side];
@@ -861,6 +902,7 @@ struct Solver {
       return;
     }
     B* first_basis;  // d1 (rect) or l1 (square)
+    swap_perm(0, 0);
     if (square) {
       set_pos_and_unit(tpos.as<long long>(), PL.as<T>(), idx);
       set_pivot(pv.as<T>(), beta);
@@ -882,6 +924,7 @@ struct Solver {
         trivial();
         return;
       }
+      swap_perm(1, 0);
       set_pos_and_unit(gpos.as<long long>(), PL.as<T>(), idx2);
       set_pivot(pv.as<T>() + 1, alpha);
       normalize_kernel<T, B><<<grid_for(ldn, 256, NORM_G), 256, 0, s>>>(n, ldn, q.as<T>(), pv.as<T>() + 1, Lcol(0), st, 1, 0);
@@ -896,16 +939,28 @@ struct Solver {
       CK(cudaMemcpyAsync(Wcol(0), &w00d, sizeof(double), cudaMemcpyHostToDevice, s));
     }
     // sketch setup (solvers.py:454-463)
-    S2->apply(r0.p, wdt, sr0.as<double>());
-    sk0++;
-    if (sb) {
-      S2->apply(first_basis, bdt, Gb.as<double>());
+    if (skd) {
+      S2->apply(r0.p, wdt, sr0.as<double>());
       sk0++;
+      if (sb) {
+        S2->apply(first_basis, bdt, Gb.as<double>());
+        sk0++;
+      }
+      if (lamon) {
+        S1->apply(Lcol(0), bdt, Fb.as<double>());
+        sk0++;
+      }
+    } else {
+      // rhs = beta e1 (solvers.py:502-504); N = I_k (506-508) as columns e_j
+      CK(cudaMemcpyAsync(sr0.p, &beta, sizeof(double), cudaMemcpyHostToDevice, s));
+      if (lamon) {
+        std::vector<double> eye((size_t)ell * (K + 1), 0.0);
+        for (int j = 0; j <= K && j < ell; ++j) eye[(size_t)j * ell + j] = 1.0;
+        CK(cudaMemcpy(Fb.p, eye.data(), eye.size() * sizeof(double), cudaMemcpyHostToDevice));
+      }
+      CK(cudaStreamSynchronize(s));
     }
-    if (lamon) {
-      S1->apply(Lcol(0), bdt, Fb.as<double>());
-      sk0++;
-    }
+    (void)first_basis;
 
     if (timing) CK(cudaStreamSynchronize(s));
     const auto t_init = now();
@@ -946,7 +1001,7 @@ struct Solver {
     // basis work; u is not overwritten by the elimination (it writes u2), the
     // next A-apply waits for the sketch to have read u, and the fused iterate
     // of iteration k+1 waits for y^{(k)}.
-    const bool ovl = !sb;
+    const bool ovl = skd && !sb;
     cudaStream_t s2 = ovl ? ctx->aux : s;
     DBuf u2(ovl ? ldm * sizeof(T) : 0);
     T* uel = ovl ? u2.as<T>() : u.as<T>();  // elimination output on the side that is sketched
@@ -996,9 +1051,14 @@ struct Solver {
       if (!square) {
         fsub(u.as<T>(), tpos.as<long long>(), PD.as<T>(), ldp, k, k, 0, cvec.as<T>(), Hcol(k - 1));
         elim(u.as<T>(), m, ldm, D, k, 0, k, 0, nullptr, nullptr, uel);
+        sample(uel, m, k, 2 * k, 0, k);
         pivot_commit_kernel<T, B><<<1, 256, 0, s>>>(k, m, Hcol(k - 1), tpos.as<long long>(), PD.as<T>(), ldp, D, ldm,
                                                     0, m, st, 0, k, pv.as<T>());
         CKL();
+        swap_perm(0, k);
+        if (!skd)
+          CK(cudaMemcpyAsync(Zb.as<double>() + (long long)(k - 1) * ell, Hcol(k - 1), (size_t)(k + 1) * sizeof(double),
+                             cudaMemcpyDeviceToDevice, s));
         normalize_kernel<T, B><<<grid_for(ldm, 256, NORM_G), 256, 0, s>>>(m, ldm, uel, pv.as<T>(), Dcol(k), st, 0, k);
         CKL();
         if (sb) S2->apply(Dcol(k), bdt, Gb.as<double>() + (long long)k * ell);
@@ -1006,19 +1066,26 @@ struct Solver {
         fsub(q.as<T>(), gpos.as<long long>(), PL.as<T>(), ldp, k, k, 1, cvec.as<T>(), Wcol(k));
         wait_y();
         elim(q.as<T>(), n, ldn, L, k, 1, k, kx, yprev, relslot, q.as<T>());
+        sample(q.as<T>(), n, k, 2 * k + 1, 1, k);
         pivot_commit_kernel<T, B><<<1, 256, 0, s>>>(k, n, Wcol(k), gpos.as<long long>(), PL.as<T>(), ldp, L, ldn, 0,
                                                     n, st, 1, k, pv.as<T>() + 1);
         CKL();
+        swap_perm(1, k);
         normalize_kernel<T, B><<<grid_for(ldn, 256, NORM_G), 256, 0, s>>>(n, ldn, q.as<T>(), pv.as<T>() + 1, Lcol(k), st, 1, k);
         CKL();
       } else {
-        if (!ovl && !sb) S2->apply(u.p, wdt, Zb.as<double>() + (long long)(k - 1) * ell);
+        if (skd && !ovl && !sb) S2->apply(u.p, wdt, Zb.as<double>() + (long long)(k - 1) * ell);
         fsub(u.as<T>(), tpos.as<long long>(), PL.as<T>(), ldp, k, k, 0, cvec.as<T>(), Hcol(k - 1));
         wait_y();
         elim(u.as<T>(), n, ldn, L, k, 0, k, kx, yprev, relslot, uel);
+        sample(uel, n, k, k, 0, k);
         pivot_commit_kernel<T, B><<<1, 256, 0, s>>>(k, n, Hcol(k - 1), tpos.as<long long>(), PL.as<T>(), ldp, L, ldn,
                                                     0, n, st, 0, k, pv.as<T>());
         CKL();
+        swap_perm(0, k);
+        if (!skd)
+          CK(cudaMemcpyAsync(Zb.as<double>() + (long long)(k - 1) * ell, Hcol(k - 1), (size_t)(k + 1) * sizeof(double),
+                             cudaMemcpyDeviceToDevice, s));
         normalize_kernel<T, B><<<grid_for(ldn, 256, NORM_G), 256, 0, s>>>(n, ldn, uel, pv.as<T>(), Lcol(k), st, 0, k);
         CKL();
         if (sb) S2->apply(Lcol(k), bdt, Gb.as<double>() + (long long)k * ell);
@@ -1045,7 +1112,7 @@ struct Solver {
           CK(cudaEventRecord(ev_l, s));
           CK(cudaStreamWaitEvent(s2, ev_l, 0));
         }
-        S1->apply(Lcol(k), bdt, Fb.as<double>() + (long long)k * ell, s2);
+        if (skd) S1->apply(Lcol(k), bdt, Fb.as<double>() + (long long)k * ell, s2);
       }
       CK(cudaEventRecord(ev[k], s));
       CK(cudaMemcpyAsync(hflag + k, &st->bd_iter, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1166,8 +1233,10 @@ struct Solver {
       const bool grewD = !(last && bd_at && (square || hst.bd_side == 0));
       const bool grewL = !(last && bd_at);
       if (!square && grewD) tm += 1;              // q = A^T d_{k+1}
-      sk += sb ? (grewD ? 1 : 0) : 1;             // G or Z column
-      if (lamon && grewL) sk += 1;                // F column
+      if (skd) {
+        sk += sb ? (grewD ? 1 : 0) : 1;           // G or Z column
+        if (lamon && grewL) sk += 1;              // F column
+      }
       res->matvecs[k - 1] = matvec0 + k;
       res->tmatvecs[k - 1] = tm;
       res->sketches[k - 1] = sk;

@@ -405,4 +405,49 @@ __global__ void convert_kernel(long long n, const From* __restrict__ src, To* __
     dst[e] = cvt<To>(src[e]);
 }
 
+// --------------------------------------------------------------------------
+// sampled pivoting (hessenberg.py:93-124).  The host draws the positions
+// rng.choice(pop, s, replace=False) into the admissible list perm[used:]
+// (the reference's swap-ordered t[k:] / g[k:]); among those entries the one
+// of largest |v| (ties -> smallest index) replaces the full-scan winner the
+// elimination pass left in st.  If every sampled entry is zero the full scan
+// stands: that is the reference's fallback rescan (hessenberg.py:118-124),
+// and it is a global scan because earlier pivot entries are exactly zero.
+template <class T>
+__global__ void __launch_bounds__(256)
+sample_pick_kernel(const T* __restrict__ v, const long long* __restrict__ perm, long long used,
+                   const long long* __restrict__ posn, int s, LoopState* __restrict__ st, int side, int iter) {
+  if (iter > 0) {
+    if (st->bd_iter != 0 && st->bd_iter < iter) return;
+    if (side == 1 && st->bd_iter == iter) return;
+  }
+  __shared__ Cand scratch[32];
+  Cand best{-1.0, 0.0, 0x7fffffffffffffffLL};
+  for (int i = threadIdx.x; i < s; i += blockDim.x) {
+    const long long idx = perm[used + posn[i]];
+    const double mg = (double)absval(v[idx]);
+    if (better(mg, idx, best.mag, best.idx)) best = Cand{mg, (double)v[idx], idx};
+  }
+  best = block_argmax(best, scratch);
+  if (threadIdx.x == 0 && best.mag > 0.0) {
+    st->piv_val[side] = best.val;
+    st->piv_idx[side] = best.idx;
+  }
+}
+
+// _swap_to_position (hessenberg.py:127-129) on the device copy of t / g and
+// its inverse: the new pivot moves to position `used`.  Skipped after a
+// breakdown (no pivot was taken).
+__global__ void perm_swap_kernel(long long* __restrict__ perm, long long* __restrict__ where, long long used,
+                                 const LoopState* __restrict__ st, int side) {
+  if (st->bd_iter != 0) return;
+  const long long idx = st->piv_idx[side];
+  const long long pos = where[idx];
+  const long long other = perm[used];
+  perm[used] = idx;
+  perm[pos] = other;
+  where[idx] = used;
+  where[other] = pos;
+}
+
 }  // namespace hs

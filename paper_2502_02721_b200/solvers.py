@@ -1,8 +1,11 @@
-"""Drop-in sketched solvers: ``scmrh``, ``slslu``, ``scmrh_tikhonov``,
-``slslu_tikhonov`` with the reference's signatures and result types
-(solvers.py:88-160, 562-605), running the whole iteration loop on the B200
-through one C-ABI call (``hs_solve``, restating ``_hessenberg_solve``,
-solvers.py:410-539).
+"""Drop-in Hessenberg solvers: the sketched ``scmrh``, ``slslu``,
+``scmrh_tikhonov``, ``slslu_tikhonov`` and the unsketched ``cmrh``, ``lslu``
+with the reference's signatures and result types (solvers.py:88-160,
+542-605), running the whole iteration loop on the B200 through one C-ABI call
+(``hs_solve``, restating ``_hessenberg_solve``, solvers.py:410-539).  Full and
+sampled pivoting (``PivotStrategy.sampled``, hessenberg.py:48-124) both run on
+the device; for the sampled strategy the host draws the positions with the
+reference's ``default_rng(seed).choice`` sequence before the loop.
 
 Device knobs added to :class:`SolverConfig` (defaults reproduce the reference):
 
@@ -17,9 +20,8 @@ Device knobs added to :class:`SolverConfig` (defaults reproduce the reference):
 * ``record_rel_err`` -- compute rel_err at every iteration (default True when
                       x_true is given, as the reference does)
 
-Out of scope in this version (raise NotImplementedError): the unsketched
-CMRH/LSLU and the GMRES/LSQR references, ``compute_diagnostics=True``,
-sampled pivoting, ``printed_f_columns=True``.
+Out of scope in this version (raise NotImplementedError): the GMRES/LSQR
+references, ``compute_diagnostics=True``, ``printed_f_columns=True``.
 """
 
 from __future__ import annotations
@@ -51,6 +53,8 @@ __all__ = [
     "slslu",
     "scmrh_tikhonov",
     "slslu_tikhonov",
+    "cmrh",
+    "lslu",
     "SOLVERS",
 ]
 
@@ -226,15 +230,35 @@ def _default_sketch(cfg, ell, in_rows, seed):
     return SparseSignSketch(ell, in_rows, seed, cfg.sketch_zeta)
 
 
-def _hessenberg_solve(A, b, cfg, x_true, square, sketch_basis, sketch=None, S1=None):
-    """solvers.py:410-539, sketched branch, on the device."""
+def pivot_positions(strategy, maxiter, rows, cols, square):
+    """The draws of the sampled strategy in the reference's order
+    (hessenberg.py:171-173, 289-301, 214, 352, 376): one slot per selection,
+    ``default_rng(seed).choice(pop, s, replace=False)`` whenever s < pop.
+    ``rng.choice(t[k:], s)`` equals ``t[k:][rng.choice(pop, s)]`` with the
+    same generator state afterwards, so positions suffice; the device maps
+    them through its copy of the swap-ordered permutation."""
+    s = int(strategy.sample_size)
+    rng = np.random.default_rng(strategy.seed)
+    if square:
+        pops = [rows] + [rows - k for k in range(1, maxiter + 1)]
+    else:
+        pops = [rows, cols]
+        for k in range(1, maxiter + 1):
+            pops += [rows - k, cols - k]
+    out = np.full((len(pops), s), -1, dtype=np.int64)
+    for slot, pop in enumerate(pops):
+        if pop > 0 and s < pop:
+            out[slot] = rng.choice(pop, size=s, replace=False)
+    return out
+
+
+def _hessenberg_solve(A, b, cfg, x_true, square, sketch_basis, sketch=None, S1=None, sketched=True):
+    """solvers.py:410-539 on the device (sketched or unsketched branch)."""
     cfg = cfg or SolverConfig()
     if square and not A.is_square:
         raise ValueError("this solver needs a square operator")
     if cfg.compute_diagnostics:
         raise NotImplementedError("compute_diagnostics is out of scope for the device path")
-    if cfg.pivot.kind != "full":
-        raise NotImplementedError("sampled pivoting is not implemented on the device yet")
     b = np.ascontiguousarray(b, dtype=np.float64)
     if b.shape != (A.rows,):
         raise ValueError(f"b must have length {A.rows}, got shape {b.shape}")
@@ -243,7 +267,13 @@ def _hessenberg_solve(A, b, cfg, x_true, square, sketch_basis, sketch=None, S1=N
         # hessenberg.py:171-173 / 290-291: zero initial residual, no iteration
         return SolveResult(x=np.zeros(A.cols), trace=SolverTrace(), termination="trivial")
     dev = to_device_operator(A)
-    if sketch is not None:
+    positions = None
+    if cfg.pivot.kind == "sampled":
+        positions = pivot_positions(cfg.pivot, cfg.maxiter, A.rows, A.cols, square)
+    if not sketched:
+        ell = cfg.maxiter + 1
+        S2 = S1 = None
+    elif sketch is not None:
         if sketch.in_rows != A.rows:
             raise ValueError(
                 f"sketch expects vectors of length {sketch.in_rows}, operator produces length {A.rows}"
@@ -251,16 +281,17 @@ def _hessenberg_solve(A, b, cfg, x_true, square, sketch_basis, sketch=None, S1=N
         ell = sketch.out_rows
     else:
         ell = cfg.effective_sketch_rows()
-    if ell < cfg.maxiter + 1:
-        raise ValueError(
-            f"sketch_rows={ell} cannot embed a {cfg.maxiter}-dimensional projected problem; "
-            "need at least maxiter+1 rows"
-        )
-    S2 = device_sketch(sketch) if sketch is not None else _default_sketch(cfg, ell, A.rows, cfg.seed)
-    if cfg.lam > 0.0:
-        S1 = device_sketch(S1) if S1 is not None else _default_sketch(cfg, ell, A.cols, derive_seed(cfg.seed, 1))
-    else:
-        S1 = None
+    if sketched:
+        if ell < cfg.maxiter + 1:
+            raise ValueError(
+                f"sketch_rows={ell} cannot embed a {cfg.maxiter}-dimensional projected problem; "
+                "need at least maxiter+1 rows"
+            )
+        S2 = device_sketch(sketch) if sketch is not None else _default_sketch(cfg, ell, A.rows, cfg.seed)
+        if cfg.lam > 0.0:
+            S1 = device_sketch(S1) if S1 is not None else _default_sketch(cfg, ell, A.cols, derive_seed(cfg.seed, 1))
+        else:
+            S1 = None
     if x_true is not None:
         x_true = np.ascontiguousarray(x_true, dtype=np.float64)
     basis_dtype = cfg.basis_dtype or cfg.dtype
@@ -270,9 +301,12 @@ def _hessenberg_solve(A, b, cfg, x_true, square, sketch_basis, sketch=None, S1=N
         maxiter=cfg.maxiter, square=1 if square else 0, sketch_basis=1 if sketch_basis else 0,
         work_dtype=_lib.DTYPE_CODES[cfg.dtype], basis_dtype=_lib.DTYPE_CODES[basis_dtype],
         record_x=1 if (x_true is not None and cfg.record_rel_err) else 0, lam=float(cfg.lam),
+        sketched=1 if sketched else 0, pivot_sample=0 if positions is None else int(cfg.pivot.sample_size),
+        pivot_positions=None if positions is None else positions.ctypes.data,
     )
     h = _lib.c_vp()
-    _lib.check(_lib.load().hs_solve(dev.ctx.handle, dev.handle, ctypes.byref(hc), S2.handle,
+    _lib.check(_lib.load().hs_solve(dev.ctx.handle, dev.handle, ctypes.byref(hc),
+                                    S2.handle if S2 is not None else None,
                                     S1.handle if S1 is not None else None, _lib.ptr(b), _lib.ptr(x0),
                                     _lib.ptr(x_true), ctypes.byref(h)))
     nr = _NativeResult(h, A.rows, A.cols, ell)
@@ -284,7 +318,7 @@ def _hessenberg_solve(A, b, cfg, x_true, square, sketch_basis, sketch=None, S1=N
         rel = float(nr.relerr[i])
         trace.records.append(TraceRecord(
             iteration=i + 1,
-            sres_norm=float(nr.sres[i]),
+            sres_norm=float(nr.sres[i]) if sketched else None,
             proj_obj=float(nr.proj[i]),
             rel_err=None if (x_true is None or np.isnan(rel)) else rel,
             matvecs=int(nr.matvecs[i]), tmatvecs=int(nr.tmatvecs[i]), dots=int(nr.dots[i]),
@@ -317,7 +351,20 @@ def slslu_tikhonov(A, b, cfg=None, x_true=None, *, printed_f_columns=False):
     return _hessenberg_solve(A, b, cfg, x_true, False, False)
 
 
+def cmrh(A, b, cfg=None, x_true=None):
+    """Quasi-minimal residual on the pivoted Hessenberg basis (solvers.py:542-550):
+    min |beta e1 - H_{k+1,k} y| (+ lam^2 |y|^2), x = L_k y."""
+    return _hessenberg_solve(A, b, cfg, x_true, True, False, sketched=False)
+
+
+def lslu(A, b, cfg=None, x_true=None):
+    """Quasi-minimal residual on the generalized Hessenberg bases (solvers.py:553-559)."""
+    return _hessenberg_solve(A, b, cfg, x_true, False, False, sketched=False)
+
+
 SOLVERS = {
+    "cmrh": cmrh,
+    "lslu": lslu,
     "scmrh": scmrh,
     "slslu": slslu,
 }

@@ -25,6 +25,7 @@ import hessketch  # noqa: E402
 from hessketch import problems, solvers  # noqa: E402
 from hessketch.hessenberg import (  # noqa: E402
     GeneralizedHessenbergState,
+    PivotStrategy,
     init_generalized,
     init_square,
     step_generalized,
@@ -254,6 +255,64 @@ def gen_edge():
     _save("edge_cases", **o)
 
 
+def gen_sampled_and_unsketched():
+    """Sampled pivoting (PivotStrategy.sampled, hessenberg.py:48-124) and the
+    unsketched cmrh / lslu (solvers.py:542-559), dense and tomography."""
+    o = {}
+    rng = np.random.default_rng(303)
+    n = 40
+    M = rng.standard_normal((n, n)) + 4.0 * np.eye(n)
+    b = rng.standard_normal(n)
+    x_true = np.linalg.solve(M, b)
+    A = LinearOperator.from_matrix(M)
+    o.update(sq_M=M, sq_b=b, sq_x_true=x_true)
+    # sampled scmrh (Gaussian S2 from cfg.seed)
+    cfg = solvers.SolverConfig(maxiter=15, seed=5, pivot=PivotStrategy.sampled(5, seed=13))
+    o["samp_sq_S2"] = make_gaussian_sketch(cfg.effective_sketch_rows(), n, 5).entries
+    o.update(_pack_result(solvers.scmrh(A, b, cfg, x_true=x_true), "samp_sq_"))
+    # unsketched cmrh, lam = 0 and lam > 0
+    o.update(_pack_result(solvers.cmrh(A, b, solvers.SolverConfig(maxiter=15), x_true=x_true), "cmrh_"))
+    o.update(_pack_result(solvers.cmrh(A, b, solvers.SolverConfig(maxiter=12, lam=0.3), x_true=x_true), "cmrh_tik_"))
+    # sampled cmrh on a banded operator with a sparse right-hand side: the
+    # sampled subsets miss every nonzero early on (full-scan fallback)
+    Mb = np.diag(np.full(n, 3.0)) + np.diag(np.full(n - 1, -1.0), 1) + np.diag(np.full(n - 1, 0.5), -1)
+    bb = np.zeros(n)
+    bb[7] = 1.0
+    o.update(band_M=Mb, band_b=bb)
+    o.update(_pack_result(
+        solvers.cmrh(LinearOperator.from_matrix(Mb), bb, solvers.SolverConfig(maxiter=10, pivot=PivotStrategy.sampled(3, seed=4))),
+        "band_"))
+    # rectangular: sampled slslu, unsketched lslu (lam 0 / > 0), sampled lslu
+    rng = np.random.default_rng(404)
+    m, nn = 60, 25
+    Mr = rng.standard_normal((m, nn))
+    br = rng.standard_normal(m)
+    xr = np.linalg.lstsq(Mr, br, rcond=None)[0]
+    Ar = LinearOperator.from_matrix(Mr)
+    o.update(re_M=Mr, re_b=br, re_x_true=xr)
+    cfg = solvers.SolverConfig(maxiter=12, seed=7, pivot=PivotStrategy.sampled(4, seed=2))
+    o["samp_re_S2"] = make_gaussian_sketch(cfg.effective_sketch_rows(), m, 7).entries
+    o.update(_pack_result(solvers.slslu(Ar, br, cfg, x_true=xr), "samp_re_"))
+    o.update(_pack_result(solvers.lslu(Ar, br, solvers.SolverConfig(maxiter=12), x_true=xr), "lslu_"))
+    o.update(_pack_result(solvers.lslu(Ar, br, solvers.SolverConfig(maxiter=10, lam=0.5), x_true=xr), "lslu_tik_"))
+    o.update(_pack_result(
+        solvers.lslu(Ar, br, solvers.SolverConfig(maxiter=10, pivot=PivotStrategy.sampled(6, seed=1)), x_true=xr),
+        "lslu_samp_"))
+    # tomography 16^2 x 12 angles: sampled sLSLU through sketch= (sparse-sign), unsketched LSLU
+    prob = problems.make_tomography(16, 12, noise_level=0.01, seed=4)
+    K = problems.tomography_matrix(16, 12)
+    S = sparse_sign_entries(60, K.shape[0], 8, seed=9)
+    sk = SketchOperator(60, K.shape[0], seed=9, entries=S)
+    o.update(tomo_b=prob.b, tomo_x_true=prob.x_true)
+    o.update(_csr_arrays(S, prefix="tomo_S2_"))
+    o.update(_pack_result(
+        solvers.slslu(prob.operator, prob.b, solvers.SolverConfig(maxiter=30, pivot=PivotStrategy.sampled(25, seed=8)),
+                      x_true=prob.x_true, sketch=sk), "tomo_samp_"))
+    o.update(_pack_result(solvers.lslu(prob.operator, prob.b, solvers.SolverConfig(maxiter=30), x_true=prob.x_true),
+                          "tomo_lslu_"))
+    _save("sampled_unsketched", **o)
+
+
 if __name__ == "__main__":
     print("reference hessketch", hessketch.__version__)
     gen_pivot_and_steps()
@@ -262,3 +321,4 @@ if __name__ == "__main__":
     gen_tomography()
     gen_deblur()
     gen_edge()
+    gen_sampled_and_unsketched()

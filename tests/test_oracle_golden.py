@@ -218,3 +218,39 @@ def test_oracle32_tracks_oracle64(golden):
     np.testing.assert_array_equal(t64, t32)
     np.testing.assert_array_equal(g64, g32)
     np.testing.assert_allclose(r32.x, r64.x, rtol=1e-3, atol=1e-4 * np.abs(r64.x).max())
+
+
+def test_sampled_pivoting_and_unsketched_bitwise(golden):
+    """Sampled pivoting (hessenberg.py:93-124, rng.choice over the swap-ordered
+    admissible list, full-scan fallback on an all-zero sample) and the
+    unsketched cmrh / lslu (solvers.py:542-559) against the reference."""
+    g = golden("sampled_unsketched")
+    A = ho.dense_operator(g["sq_M"], sequential=False)
+    b, xt = g["sq_b"], g["sq_x_true"]
+    res = ho.hessenberg_solve(A, b, square=True, maxiter=15, seed=5, x_true=xt, pivot_sample=5, pivot_seed=13)
+    _check_result(res, g, "samp_sq_")
+    res = ho.hessenberg_solve(A, b, square=True, maxiter=15, x_true=xt, sketched=False)
+    _check_result(res, g, "cmrh_")
+    res = ho.hessenberg_solve(A, b, square=True, maxiter=12, lam=0.3, x_true=xt, sketched=False)
+    _check_result(res, g, "cmrh_tik_")
+    Ab = ho.dense_operator(g["band_M"], sequential=False)
+    res = ho.hessenberg_solve(Ab, g["band_b"], square=True, maxiter=10, sketched=False, pivot_sample=3, pivot_seed=4)
+    _check_result(res, g, "band_")
+    Ar = ho.dense_operator(g["re_M"], sequential=False)
+    b, xt = g["re_b"], g["re_x_true"]
+    res = ho.hessenberg_solve(Ar, b, square=False, maxiter=12, seed=7, x_true=xt, pivot_sample=4, pivot_seed=2)
+    _check_result(res, g, "samp_re_")
+    res = ho.hessenberg_solve(Ar, b, square=False, maxiter=12, x_true=xt, sketched=False)
+    _check_result(res, g, "lslu_")
+    res = ho.hessenberg_solve(Ar, b, square=False, maxiter=10, lam=0.5, x_true=xt, sketched=False)
+    _check_result(res, g, "lslu_tik_")
+    res = ho.hessenberg_solve(Ar, b, square=False, maxiter=10, x_true=xt, sketched=False, pivot_sample=6, pivot_seed=1)
+    _check_result(res, g, "lslu_samp_")
+    K = _csr(golden("tomo_matrices"), "tomo16x12_")
+    At = ho.csr_operator(K)
+    S2 = _csr(g, "tomo_S2_")
+    res = ho.hessenberg_solve(At, g["tomo_b"], square=False, maxiter=30, S2=S2, x_true=g["tomo_x_true"],
+                              pivot_sample=25, pivot_seed=8)
+    _check_result(res, g, "tomo_samp_")
+    res = ho.hessenberg_solve(At, g["tomo_b"], square=False, maxiter=30, x_true=g["tomo_x_true"], sketched=False)
+    _check_result(res, g, "tomo_lslu_")
