@@ -1001,7 +1001,7 @@ struct Solver {
     // basis work; u is not overwritten by the elimination (it writes u2), the
     // next A-apply waits for the sketch to have read u, and the fused iterate
     // of iteration k+1 waits for y^{(k)}.
-    const bool ovl = skd && !sb;
+    const bool ovl = skd && !sb && !env_flag("HS_NO_OVERLAP");  // knob: serialise for A/B
     cudaStream_t s2 = ovl ? ctx->aux : s;
     DBuf u2(ovl ? ldm * sizeof(T) : 0);
     T* uel = ovl ? u2.as<T>() : u.as<T>();  // elimination output on the side that is sketched

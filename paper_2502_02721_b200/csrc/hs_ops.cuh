@@ -416,25 +416,71 @@ __global__ void sell_delta_fill_kernel(long long rows, long long nslices, const 
   if (len == 0 && row < rows) rbase[row] = 0;
 }
 
-template <class Tin>
-__device__ __forceinline__ const Tin* pick_x(const Tin* xrow, const Tin* xT, const unsigned char* sflag, long long s) {
-  return (sflag != nullptr && sflag[s]) ? xT : xrow;
-}
-
-// column index in the gathered vector: image order, or transposed for flagged slices
-__device__ __forceinline__ int tidx(int c, bool tr, int grid, int gshift) {
-  if (!tr) return c;
-  if (gshift >= 0) return ((c & (grid - 1)) << gshift) | (c >> gshift);
+// gather position of image column c: GM 0 = as stored, 1 = transposed with
+// grid = 2^sh (m = grid - 1), 2 = transposed, general grid
+template <int GM>
+__device__ __forceinline__ int gpos(int c, int m, int sh, int grid) {
+  if (GM == 0) return c;
+  if (GM == 1) return ((c & m) << sh) | (c >> sh);
   return (c % grid) * grid + c / grid;
 }
 
-// gather index of column c: identity, or the transposed-image position.
-// POW2 (grid = 2^sh): branch-free  ((c & m) << sh) | (c >> sh)  with
-// (m, sh) = (-1, 0) for image-order slices and (grid-1, log2 grid) otherwise.
-template <bool POW2>
-__device__ __forceinline__ int gidx(int c, int m, int sh, bool tr, int grid) {
-  if (POW2) return ((c & m) << sh) | (c >> sh);
-  return tr ? (c % grid) * grid + c / grid : c;
+// one full chunk of a lane's row: decode 4 deltas, 4 gathers, 4 ordered adds
+template <int GM, class V, class Tin, class T>
+__device__ __forceinline__ void d16_chunk(T& acc, int& c, const int2 d, const Chunk4<V>& v, const Tin* __restrict__ x,
+                                          int m, int sh, int grid) {
+  const int c0 = c + (int)(short)(d.x & 0xffff);
+  const int c1 = c0 + (d.x >> 16);
+  const int c2 = c1 + (int)(short)(d.y & 0xffff);
+  const int c3 = c2 + (d.y >> 16);
+  const T x0 = gather_x<T>(x, gpos<GM>(c0, m, sh, grid));
+  const T x1 = gather_x<T>(x, gpos<GM>(c1, m, sh, grid));
+  const T x2 = gather_x<T>(x, gpos<GM>(c2, m, sh, grid));
+  const T x3 = gather_x<T>(x, gpos<GM>(c3, m, sh, grid));
+  acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[0]), x0));
+  acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[1]), x1));
+  acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[2]), x2));
+  acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[3]), x3));
+  c = c3;
+}
+
+template <int GM, class V, class Tin, class T>
+__device__ __forceinline__ void d16_tail(T& acc, int c, const int2 d, const Chunk4<V>& v, int rem,
+                                         const Tin* __restrict__ x, int m, int sh, int grid) {
+  const int c0 = c + (int)(short)(d.x & 0xffff);
+  const int c1 = c0 + (d.x >> 16);
+  const int c2 = c1 + (int)(short)(d.y & 0xffff);
+  acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[0]), gather_x<T>(x, gpos<GM>(c0, m, sh, grid))));
+  if (rem > 1) acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[1]), gather_x<T>(x, gpos<GM>(c1, m, sh, grid))));
+  if (rem > 2) acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[2]), gather_x<T>(x, gpos<GM>(c2, m, sh, grid))));
+}
+
+// One lane's row: one chunk of (delta, value) prefetched ahead; the gathers
+// are issued as soon as a chunk's columns are decoded.  (Measured: a deeper
+// per-lane pipeline, or two alternating register buffers, cost registers,
+// i.e. spills or resident warps, and ran 2-3% slower.)
+template <int GM, class V, class Tin, class T>
+__device__ __forceinline__ T d16_row(const short* __restrict__ dp, const V* __restrict__ vp, int c, int len,
+                                     const Tin* __restrict__ x, int m, int sh, int grid) {
+  T acc = T(0);
+  const int nq = (len + 3) >> 2, nfull = len >> 2;
+  if (nq == 0) return acc;
+  int2 d = __ldcs(reinterpret_cast<const int2*>(dp));
+  Chunk4<V> v = Chunk4<V>::load(vp);
+  for (int q = 0; q < nfull; ++q) {
+    int2 dn = d;
+    Chunk4<V> vn = v;
+    if (q + 1 < nq) {
+      dn = __ldcs(reinterpret_cast<const int2*>(dp + (long long)(q + 1) * 128));
+      vn = Chunk4<V>::load(vp + (long long)(q + 1) * 128);
+    }
+    d16_chunk<GM>(acc, c, d, v, x, m, sh, grid);
+    d = dn;
+    v = vn;
+  }
+  const int rem = len & 3;
+  if (rem) d16_tail<GM>(acc, c, d, v, rem, x, m, sh, grid);
+  return acc;
 }
 
 template <class V, class Tin, class T, bool POW2>
@@ -453,58 +499,18 @@ sell_spmv_d16_kernel(long long rows, long long nslices, const long long* __restr
     i = __shfl_sync(0xffffffffu, i, 0);
     if (i >= nslices) break;
     const long long s = sorder ? (long long)sorder[i] : (long long)i;
-    const bool tr = sflag != nullptr && sflag[s];
-    const Tin* __restrict__ x = tr ? xT : xrow;
-    const int m = tr ? grid - 1 : -1, sh = tr ? gshift : 0;
+    const bool tr = sflag != nullptr && sflag[s];  // warp-uniform: one specialised row loop each
     const long long slot = s * 32 + lane;  // rlen / rbase are slot-indexed; rperm maps slot -> row
     const long long row = rperm ? (long long)rperm[slot] : slot;
     const int len = rlen[slot];
-    int c = rbase[slot];
+    const int c = rbase[slot];
     const long long base = sptr[s];
-    const int nq = (len + 3) >> 2, nfull = len >> 2;
     const short* dp = dcol + base + lane * 4;
     const V* vp = val + base + lane * 4;
-    T acc = T(0);
-    if (nq > 0) {
-      // one chunk of (delta, value) prefetched ahead; gathers issued as soon
-      // as a chunk's columns are decoded (a deeper per-lane pipeline costs
-      // registers, i.e. resident warps, and measured slower)
-      int2 d = __ldcs(reinterpret_cast<const int2*>(dp));
-      Chunk4<V> v = Chunk4<V>::load(vp);
-      // full chunks: no per-entry predicates
-      for (int q = 0; q < nfull; ++q) {
-        int2 dn = d;
-        Chunk4<V> vn = v;
-        if (q + 1 < nq) {
-          dn = __ldcs(reinterpret_cast<const int2*>(dp + (long long)(q + 1) * 128));
-          vn = Chunk4<V>::load(vp + (long long)(q + 1) * 128);
-        }
-        const int c0 = c + (int)(short)(d.x & 0xffff);
-        const int c1 = c0 + (d.x >> 16);
-        const int c2 = c1 + (int)(short)(d.y & 0xffff);
-        const int c3 = c2 + (d.y >> 16);
-        const T x0 = gather_x<T>(x, gidx<POW2>(c0, m, sh, tr, grid));
-        const T x1 = gather_x<T>(x, gidx<POW2>(c1, m, sh, tr, grid));
-        const T x2 = gather_x<T>(x, gidx<POW2>(c2, m, sh, tr, grid));
-        const T x3 = gather_x<T>(x, gidx<POW2>(c3, m, sh, tr, grid));
-        acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[0]), x0));
-        acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[1]), x1));
-        acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[2]), x2));
-        acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[3]), x3));
-        c = c3;
-        d = dn;
-        v = vn;
-      }
-      const int rem = len & 3;
-      if (rem) {  // tail chunk (already loaded into d / v)
-        const int c0 = c + (int)(short)(d.x & 0xffff);
-        const int c1 = c0 + (d.x >> 16);
-        const int c2 = c1 + (int)(short)(d.y & 0xffff);
-        acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[0]), gather_x<T>(x, gidx<POW2>(c0, m, sh, tr, grid))));
-        if (rem > 1) acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[1]), gather_x<T>(x, gidx<POW2>(c1, m, sh, tr, grid))));
-        if (rem > 2) acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[2]), gather_x<T>(x, gidx<POW2>(c2, m, sh, tr, grid))));
-      }
-    }
+    T acc;
+    if (!tr) acc = d16_row<0, V, Tin, T>(dp, vp, c, len, xrow, 0, 0, grid);
+    else if (POW2) acc = d16_row<1, V, Tin, T>(dp, vp, c, len, xT, grid - 1, gshift, grid);
+    else acc = d16_row<2, V, Tin, T>(dp, vp, c, len, xT, 0, 0, grid);
     if (row >= 0 && row < rows) y[row] = acc;
   }
   // the last warp out resets the scheduler for the next launch
