@@ -36,6 +36,10 @@ __all__ = [
     "PsfOperator",
     "TomographyOperator",
     "to_device_operator",
+    "spectral_condition_number",
+    "save_array",
+    "load_array",
+    "load_operator",
 ]
 
 
@@ -315,3 +319,53 @@ def to_device_operator(A):
         "operator has no device implementation (Python callables are not run on the GPU); "
         "use DenseOperator / CsrOperator / PsfOperator / TomographyOperator or from_matrix"
     )
+
+
+# ---------------------------------------------------------------------------
+# exchange formats (linops.py:235-282): MatrixMarket files and the condition
+# number the reference's diagnostics report.  Host-side I/O around the device
+# path; ``load_operator`` returns a device operator.
+
+
+def spectral_condition_number(M):
+    """sigma_max / sigma_min by SVD (linops.py:235-247); inf when sigma_min
+    underflows below 1e-300; ValueError for an empty or all-zero matrix."""
+    M = np.asarray(M, dtype=float)
+    if M.ndim != 2 or M.size == 0:
+        raise ValueError("expected a nonempty 2-D matrix")
+    sv = np.linalg.svd(M, compute_uv=False)
+    if sv[0] == 0.0:
+        raise ValueError("condition number of the zero matrix is undefined")
+    return np.inf if sv[-1] < 1e-300 else float(sv[0] / sv[-1])
+
+
+def save_array(path, arr):
+    """MatrixMarket array file of a vector (one column) or matrix
+    (linops.py:249-260); the path is used verbatim."""
+    import scipy.io
+
+    a = np.asarray(arr, dtype=float)
+    a = a[:, None] if a.ndim == 1 else a
+    with open(path, "wb") as fh:
+        scipy.io.mmwrite(fh, a)
+
+
+def load_array(path):
+    """Dense array from a MatrixMarket file; single columns come back 1-D
+    (linops.py:262-271)."""
+    import scipy.io
+
+    with open(path, "rb") as fh:
+        a = scipy.io.mmread(fh)
+    a = np.asarray(a.toarray() if scipy.sparse.issparse(a) else a, dtype=float)
+    return a[:, 0].copy() if (a.ndim == 2 and a.shape[1] == 1) else a
+
+
+def load_operator(path):
+    """Device operator from a MatrixMarket file (linops.py:274-282):
+    coordinate files -> :class:`CsrOperator`, array files -> :class:`DenseOperator`."""
+    import scipy.io
+
+    with open(path, "rb") as fh:
+        M = scipy.io.mmread(fh)
+    return LinearOperator.from_matrix(M)

@@ -1,4 +1,7 @@
-"""Synthetic workloads of BASELINE.json's five configs.
+"""Problem builders: the reference's own (``make_tomography``, ``make_deblur``,
+their phantoms and PSFs, the ``Problem`` / ``Image`` bundles and 16-bit PGM
+image exchange, problems.py:61-473) with device operators, and the synthetic
+workloads of BASELINE.json's five configs.
 
 The reference ships only fixed phantoms (problems.py:155-233) and its own
 tomography geometry (detectors = grid).  BASELINE's configs ask for seeded
@@ -16,11 +19,24 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+from typing import Optional
+
 from .linops import DenseOperator, PsfOperator, TomographyOperator
 from .solvers import SolverConfig
 from .sketch import GaussianSketch, SketchOperator, SparseSignSketch, make_gaussian_sketch
 
 __all__ = [
+    "Problem",
+    "Image",
+    "ImageFormatError",
+    "motion_psf",
+    "deblur_phantom",
+    "tomography_phantom",
+    "make_deblur",
+    "make_tomography",
+    "image_from_vector",
+    "write_image",
+    "read_image",
     "Workload",
     "gaussian_psf",
     "add_noise",
@@ -61,6 +77,236 @@ def add_noise(b_clean, level, seed):
     g = np.random.default_rng(seed).standard_normal(b_clean.size)
     e = (level * scale / np.linalg.norm(g)) * g
     return b_clean + e, e
+
+
+# ---------------------------------------------------------------------------
+# the reference's problem bundles, phantoms and builders (problems.py:61-351)
+
+
+@dataclass
+class Problem:
+    """``b = A x_true + e`` (problems.py:61-99); ``operator`` is a device operator."""
+
+    operator: object
+    b: np.ndarray
+    x_true: Optional[np.ndarray] = None
+    noise_level: float = 0.0
+    seed: int = 0
+    image_shape: Optional[tuple] = None
+
+    def __post_init__(self):
+        self.b = np.asarray(self.b, dtype=float)
+        if self.b.ndim != 1 or self.b.size != self.operator.rows:
+            raise ValueError("observation length must match operator rows")
+        if self.x_true is not None:
+            self.x_true = np.asarray(self.x_true, dtype=float)
+            if self.x_true.ndim != 1 or self.x_true.size != self.operator.cols:
+                raise ValueError("ground truth length must match operator cols")
+        if self.noise_level < 0:
+            raise ValueError("noise level must be nonnegative")
+
+
+@dataclass
+class Image:
+    """Grayscale image in [0, 1], row-major ``pixels[height, width]``, row 0
+    at the top (problems.py:101-121)."""
+
+    width: int
+    height: int
+    pixels: np.ndarray
+
+    def __post_init__(self):
+        if self.width < 1 or self.height < 1:
+            raise ValueError("image dimensions must be positive")
+        self.pixels = np.asarray(self.pixels, dtype=float)
+        if self.pixels.shape != (self.height, self.width):
+            raise ValueError("pixel array must have shape (height, width)")
+        if not np.all(np.isfinite(self.pixels)):
+            raise ValueError("pixel values must be finite")
+        if self.pixels.min() < 0.0 or self.pixels.max() > 1.0:
+            raise ValueError("pixel values must lie in [0, 1]")
+
+
+class ImageFormatError(ValueError):
+    """Malformed image file; the message names a byte offset (problems.py:124-125)."""
+
+
+def motion_psf(length, angle_deg, oversample=64):
+    """Unit-mass motion-blur segment (problems.py:152-189): ``round(length *
+    oversample) + 1`` (at least 2) points along a centred segment at
+    ``angle_deg`` from the horizontal, each deposited bilinearly on the odd
+    ``2 ceil((length-1)/2) + 1`` square; axis directions snapped."""
+    if length < 1:
+        raise ValueError("length must be at least 1")
+    if not np.isfinite(angle_deg):
+        raise ValueError("angle must be finite")
+    half = math.ceil((length - 1.0) / 2.0)
+    side = 2 * half + 1
+    out = np.zeros((side, side))
+    th = math.radians(angle_deg)
+    ux, uy = math.cos(th), math.sin(th)
+    if abs(ux) < 1e-12:
+        ux = 0.0
+    if abs(uy) < 1e-12:
+        uy = 0.0
+    npts = max(2, int(round(length * oversample)) + 1)
+    span = (length - 1.0) / 2.0
+    for t in np.linspace(-span, span, npts):
+        py, px = half + t * uy, half + t * ux
+        iy, ix = int(math.floor(py)), int(math.floor(px))
+        fy, fx = py - iy, px - ix
+        taps = ((iy, ix, (1 - fy) * (1 - fx)), (iy, ix + 1, (1 - fy) * fx),
+                (iy + 1, ix, fy * (1 - fx)), (iy + 1, ix + 1, fy * fx))
+        for r, c, wgt in taps:
+            if wgt > 0 and 0 <= r < side and 0 <= c < side:
+                out[r, c] += wgt
+    return out / out.sum()
+
+
+def deblur_phantom(size):
+    """Fixed deblurring test image (problems.py:192-209): gradient background
+    0.10..0.35, rectangle 0.85, discs 0.70 / 0.05, vertical bar 0.95."""
+    s = size
+    rr, cc = np.mgrid[0:s, 0:s].astype(float)
+    img = 0.10 + 0.25 * cc / max(s - 1, 1)
+    img[int(0.15 * s): int(0.45 * s), int(0.20 * s): int(0.55 * s)] = 0.85
+    for (cy, cx, rad, val) in ((0.62, 0.40, 0.18, 0.70), (0.30, 0.70, 0.08, 0.05)):
+        img[(rr - cy * s) ** 2 + (cc - cx * s) ** 2 <= (rad * s) ** 2] = val
+    w = max(1, s // 32)
+    img[int(0.55 * s): int(0.90 * s), int(0.78 * s): int(0.78 * s) + w] = 0.95
+    return img
+
+
+def tomography_phantom(grid):
+    """Fixed absorption phantom (problems.py:212-233): discs 0.55, 1.0, 0.30
+    and a 0.0 void, painted in order on a zero background (pixel centres)."""
+    g = grid
+    rr, cc = np.mgrid[0:g, 0:g] + 0.5
+    img = np.zeros((g, g))
+    for cy, cx, rad, val in ((0.50, 0.50, 0.38, 0.55), (0.40, 0.42, 0.13, 1.00),
+                             (0.63, 0.58, 0.10, 0.30), (0.52, 0.33, 0.05, 0.00)):
+        img[(rr - cy * g) ** 2 + (cc - cx * g) ** 2 <= (rad * g) ** 2] = val
+    return img
+
+
+def make_deblur(size, psf, noise_level=0.0, seed=0):
+    """problems.py:240-273 on the device: zero-boundary convolution operator
+    (:class:`PsfOperator`, fp64; transpose = correlation), the fixed phantom,
+    b = A x_true + exact-level noise.  The stencil sums taps in a fixed order,
+    so b agrees with scipy's ``convolve2d`` to ~1e-16 relative, not bitwise
+    (SURVEY.md 8a item 7)."""
+    if size < 8:
+        raise ValueError("size must be at least 8")
+    k = np.asarray(psf, dtype=float)
+    if k.ndim != 2 or k.shape[0] % 2 == 0 or k.shape[1] % 2 == 0:
+        raise ValueError("psf must be a 2-D kernel with odd side lengths")
+    if k.shape[0] >= size or k.shape[1] >= size:
+        raise ValueError("psf support must be smaller than the image")
+    op = PsfOperator((size, size), k, dtype=np.float64)
+    x_true = deblur_phantom(size).ravel()
+    b, _ = add_noise(op.matvec(x_true), noise_level, seed)
+    return Problem(op, b, x_true, noise_level, seed, (size, size))
+
+
+def make_tomography(grid, n_angles, noise_level=0.0, seed=0):
+    """problems.py:334-350 on the device: the exact-chord parallel-beam matrix
+    (``grid`` detectors, built by the device ray tracer bit-identically to
+    ``tomography_matrix``), the fixed phantom, b = K x_true (bitwise the
+    reference's scipy product) + exact-level noise."""
+    if grid < 8:
+        raise ValueError("grid must be at least 8")
+    if n_angles < 2:
+        raise ValueError("need at least 2 angles")
+    op = TomographyOperator(grid, n_angles, dtype=np.float64)
+    x_true = tomography_phantom(grid).ravel()
+    b, _ = add_noise(op.matvec(x_true), noise_level, seed)
+    return Problem(op, b, x_true, noise_level, seed, (grid, grid))
+
+
+# ---------------------------------------------------------------------------
+# 16-bit binary PGM exchange (problems.py:377-473)
+
+
+def image_from_vector(v, height, width, clip=True):
+    """Flat solution vector -> :class:`Image` (clipped to [0, 1] by default)."""
+    px = np.asarray(v, dtype=float).reshape(height, width)
+    return Image(width=width, height=height, pixels=np.clip(px, 0.0, 1.0) if clip else px)
+
+
+def write_image(image, path):
+    """P5 PGM, maxval 65535, big-endian samples round(clip(p) * 65535)."""
+    q = np.round(np.clip(image.pixels, 0.0, 1.0) * 65535.0).astype(">u2")
+    with open(path, "wb") as fh:
+        fh.write(b"P5\n%d %d\n65535\n" % (image.width, image.height))
+        fh.write(q.tobytes())
+
+
+def _pgm_header(data):
+    """Parse the P5 header; returns (width, height, maxval, sample offset).
+    Whitespace and '#' comments separate tokens; errors name the byte offset."""
+    pos = 0
+
+    def err(what, at):
+        raise ImageFormatError(f"{what} at byte offset {at}")
+
+    def skip(p):
+        while p < len(data):
+            ch = data[p:p + 1]
+            if ch.isspace():
+                p += 1
+            elif ch == b"#":
+                while p < len(data) and data[p:p + 1] not in (b"\n", b"\r"):
+                    p += 1
+            else:
+                break
+        return p
+
+    def token(p):
+        p = skip(p)
+        q = p
+        while q < len(data) and not data[q:q + 1].isspace():
+            q += 1
+        if q == p:
+            err("unexpected end of header", p)
+        return data[p:q], p, q
+
+    tok, start, pos = token(pos)
+    if tok != b"P5":
+        err("missing P5 magic token", 0)
+    vals = []
+    for what in ("width", "height", "maximum sample value"):
+        tok, start, pos = token(pos)
+        try:
+            v = int(tok)
+        except ValueError:
+            err(f"invalid {what} {tok!r}", start)
+        if v < 1:
+            err(f"nonpositive {what}", start)
+        vals.append(v)
+    width, height, maxval = vals
+    if maxval > 65535:
+        err("maximum sample value above 65535", pos)
+    if pos >= len(data) or not data[pos:pos + 1].isspace():
+        err("missing separator before samples", pos)
+    return width, height, maxval, pos + 1
+
+
+def read_image(path):
+    """Binary PGM (P5, 8- or 16-bit samples, maxval <= 65535) -> :class:`Image`
+    scaled to [0, 1]; malformed files raise :class:`ImageFormatError`."""
+    with open(path, "rb") as fh:
+        data = fh.read()
+    width, height, maxval, off = _pgm_header(data)
+    dt = np.dtype(">u2" if maxval > 255 else "u1")
+    need = width * height * dt.itemsize
+    if len(data) - off < need:
+        raise ImageFormatError(f"truncated sample data at byte offset {len(data)}")
+    samples = np.frombuffer(data[off:off + need], dtype=dt).astype(float)
+    return Image(width=width, height=height, pixels=(samples / maxval).reshape(height, width))
+
+
+# ---------------------------------------------------------------------------
+# BASELINE workloads
 
 
 def toeplitz_blur_1d(n, sigma_frac=0.02):

@@ -313,6 +313,59 @@ def gen_sampled_and_unsketched():
     _save("sampled_unsketched", **o)
 
 
+def gen_exchange():
+    """Phantoms, motion PSFs, PGM bytes / error messages and MatrixMarket text
+    from the reference (problems.py:152-233, 377-473; linops.py:249-282)."""
+    import tempfile
+
+    import scipy.io
+    from hessketch import linops
+
+    o = dict(deblur37=problems.deblur_phantom(37), tomo29=problems.tomography_phantom(29),
+             deblur8=problems.deblur_phantom(8))
+    for i, (length, ang) in enumerate(((7, 30.0), (5, 90.0), (1, 0.0), (9.5, -20.0), (4, 45.0))):
+        o[f"motion{i}"] = problems.motion_psf(length, ang)
+        o[f"motion{i}_args"] = np.array([length, ang])
+    rng = np.random.default_rng(12)
+    px = rng.random((5, 7))
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "a.pgm")
+        problems.write_image(problems.Image(width=7, height=5, pixels=px), path)
+        o["pgm_pixels"] = px
+        o["pgm_bytes"] = np.frombuffer(open(path, "rb").read(), dtype=np.uint8)
+        good8 = b"P5 # comment\n3 2\n255\n" + bytes([0, 10, 20, 255, 128, 1])
+        bad = [b"P6\n1 1\n255\n\x00", b"P5\n0 1\n255\n\x00", b"P5\n2 2\n70000\n" + b"\x00" * 8,
+               b"P5\n2 2\n255", b"P5\n2 2\n255\n\x00", b"P5\nx 2\n255\n\x00", b"P5\n2"]
+        msgs = []
+        for i, blob in enumerate([good8] + bad):
+            fp = os.path.join(d, f"b{i}.pgm")
+            open(fp, "wb").write(blob)
+            try:
+                img = problems.read_image(fp)
+                msgs.append("ok")
+                o["pgm8_pixels"] = img.pixels
+            except problems.ImageFormatError as e:
+                msgs.append(str(e))
+            o[f"pgm_case{i}"] = np.frombuffer(blob, dtype=np.uint8)
+        o["pgm_msgs"] = np.array(msgs)
+        M = rng.standard_normal((4, 3))
+        v = rng.standard_normal(5)
+        for name, arr in (("mtx_mat", M), ("mtx_vec", v)):
+            fp = os.path.join(d, name + ".mtx")
+            linops.save_array(fp, arr)
+            o[name] = arr
+            o[name + "_bytes"] = np.frombuffer(open(fp, "rb").read(), dtype=np.uint8)
+        S = scipy.sparse.random(6, 5, density=0.4, random_state=3, format="csr")
+        fp = os.path.join(d, "coo.mtx")
+        with open(fp, "wb") as fh:
+            scipy.io.mmwrite(fh, S)
+        o["coo_bytes"] = np.frombuffer(open(fp, "rb").read(), dtype=np.uint8)
+        o["coo_dense"] = S.toarray()
+    o["cond"] = np.array([linops.spectral_condition_number(np.array([[3.0, 0.0], [0.0, 0.5]])),
+                          linops.spectral_condition_number(np.diag([1.0, 1e-301]))])
+    _save("exchange", **o)
+
+
 if __name__ == "__main__":
     print("reference hessketch", hessketch.__version__)
     gen_pivot_and_steps()
@@ -322,3 +375,4 @@ if __name__ == "__main__":
     gen_deblur()
     gen_edge()
     gen_sampled_and_unsketched()
+    gen_exchange()
