@@ -17,6 +17,7 @@
  *   hs_solve                _hessenberg_solve                        solvers.py:410-539
  *                           via scmrh / slslu / *_tikhonov           solvers.py:562-605
  *                           and cmrh / lslu (unsketched)             solvers.py:542-559
+ *   hs_solve_krylov         gmres / lsqr (comparison solvers)        solvers.py:256-403
  *   hs_result_*             SolveResult / SolverTrace / state        solvers.py:119-160,
  *                                                                    hessenberg.py:132-158, 229-272
  *
@@ -82,6 +83,8 @@ typedef struct {
      draw.  Positions index the swap-ordered admissible list t[k:] / g[k:]
      (hessenberg.py:127-129), which the device maintains.                   */
   const int64_t* pivot_positions;
+  int32_t diagnostics;   /* compute_diagnostics: exact residual |b - A x_k| per
+                            iteration (solvers.py:523-525), hs_result_resnorm  */
 } hs_config;
 
 const char* hs_last_error(void);
@@ -147,10 +150,19 @@ int hs_sketch_destroy(hs_sketch* sk);
 int hs_solve(hs_ctx* ctx, hs_op* op, const hs_config* cfg, hs_sketch* S2, hs_sketch* S1, const double* b,
              const double* x0, const double* x_true, hs_result** out);
 
+/* the reference's comparison solvers (solvers.py:256-403): method 0 = gmres
+   (square), 1 = lsqr; cfg: maxiter, work_dtype, record_x, lam (others
+   ignored).  The result has no bases / pivots; its "Hessenberg" accessor
+   returns the projected matrix (Arnoldi H or bidiagonal B, (k+1) x k). */
+int hs_solve_krylov(hs_ctx* ctx, hs_op* op, const hs_config* cfg, int32_t method, const double* b, const double* x0,
+                    const double* x_true, hs_result** out);
+
 /* result accessors */
 int hs_result_info(const hs_result* r, int32_t* n_records, int32_t* termination, int32_t* k,
                    int32_t* breakdown_side, int32_t* n_basis_data, int32_t* n_basis_sol);
 int hs_result_x(const hs_result* r, double* x);                 /* n */
+/* per record |b - A x_k| when cfg->diagnostics was set, else NaN */
+int hs_result_resnorm(const hs_result* r, double* out);
 /* per record: sres_norm, proj_obj, rel_err (NaN if no x_true), rank_fallback,
    counters (matvecs, tmatvecs, dots, sketches), wall_ms (device events) */
 int hs_result_trace(const hs_result* r, double* sres, double* proj, double* relerr, int32_t* rank_fallback,

@@ -641,3 +641,146 @@ def pivots_of(state):
     if isinstance(state, GenState):
         return state.t[: len(state.D)].copy(), state.g[: len(state.L)].copy()
     return state.t[: len(state.L)].copy(), None
+
+
+# ---------------------------------------------------------------------------
+# the reference's comparison solvers (solvers.py:256-403), restated
+
+
+def _tracked_dot(c, x, y):
+    """linops.py:152-159: one charge per inner product."""
+    c.dots += 1
+    return float(np.dot(x, y))
+
+
+def _tracked_norm(c, x):
+    """linops.py:162-165: a norm costs one inner product."""
+    c.dots += 1
+    return float(np.linalg.norm(x))
+
+
+def _krylov_record(k, M, rhs, y, lam, N, fallback, x, x_true, A, b, diagnostics, c, tic):
+    rec = dict(iteration=k, proj_obj=objective(M, rhs, y, lam, N), sres_norm=None, rel_err=None,
+               rank_fallback=fallback, res_norm=None)
+    if x_true is not None:
+        xt = np.asarray(x_true, dtype=np.float64)
+        rec["rel_err"] = float(np.linalg.norm(x - xt) / np.linalg.norm(xt))
+    if diagnostics:  # raw forward application, not counted (solvers.py:247-250)
+        rec["res_norm"] = float(np.linalg.norm(np.asarray(b, dtype=float) - np.asarray(A.forward(x), dtype=float)))
+    rec["wall_ms"] = (time.perf_counter() - tic) * 1e3
+    return rec
+
+
+def gmres(A, b, *, maxiter, lam=0.0, x0=None, x_true=None, diagnostics=False):
+    """solvers.py:256-325: Arnoldi, modified Gram-Schmidt + one
+    reorthogonalisation pass, lucky breakdown h_{k+1,k} <= 1e-14 |h|."""
+    if not A.is_square:
+        raise ValueError("gmres needs a square operator")
+    A = A.fresh()
+    c = A.counters
+    b = np.asarray(b, dtype=float)
+    x0 = None if x0 is None else np.asarray(x0, dtype=float)
+    r0 = b.copy() if x0 is None else b - A.apply(x0)
+    beta = _tracked_norm(c, r0)
+    if beta == 0.0:
+        return Result(x=np.zeros(A.cols) if x0 is None else x0.copy(), records=[], termination="trivial")
+    V = [r0 / beta]
+    h_cols = []
+    records = []
+    x = None
+    termination = "maxiter"
+    for k in range(1, min(maxiter, A.rows) + 1):
+        tic = time.perf_counter()
+        w = A.apply(V[-1])
+        h = np.empty(k + 1)
+        for j in range(k):
+            h[j] = _tracked_dot(c, V[j], w)
+            w = w - h[j] * V[j]
+        for j in range(k):
+            corr = _tracked_dot(c, V[j], w)
+            w = w - corr * V[j]
+            h[j] += corr
+        h[k] = _tracked_norm(c, w)
+        h_cols.append(h)
+        lucky = h[k] <= 1e-14 * np.linalg.norm(h)
+        if not lucky:
+            V.append(w / h[k])
+        H = np.zeros((k + 1, k))
+        for j, col in enumerate(h_cols):
+            H[: j + 2, j] = col
+        rhs = np.zeros(k + 1)
+        rhs[0] = beta
+        N = np.eye(k) if lam > 0.0 else None
+        y, fallback = projected_solve(H, rhs, lam, N)
+        x = np.column_stack(V[:k]) @ y
+        if x0 is not None:
+            x = x0 + x
+        rec = _krylov_record(k, H, rhs, y, lam, N, fallback, x, x_true, A, b, diagnostics, c, tic)
+        rec["matvecs"], rec["tmatvecs"], rec["dots"], rec["sketches"] = c.snapshot()
+        records.append(rec)
+        if lucky:
+            termination = "breakdown"
+            break
+    return Result(x=x, records=records, termination=termination)
+
+
+def lsqr(A, b, *, maxiter, lam=0.0, x0=None, x_true=None, diagnostics=False):
+    """solvers.py:328-403: Golub-Kahan with one reorthogonalisation pass on
+    both sequences; exhausted when beta <= 1e-14 alpha or alpha <= 1e-14 beta."""
+    A = A.fresh()
+    c = A.counters
+    b = np.asarray(b, dtype=float)
+    x0 = None if x0 is None else np.asarray(x0, dtype=float)
+    r0 = b.copy() if x0 is None else b - A.apply(x0)
+    zero = np.zeros(A.cols) if x0 is None else x0.copy()
+    beta1 = _tracked_norm(c, r0)
+    if beta1 == 0.0:
+        return Result(x=zero, records=[], termination="trivial")
+    U = [r0 / beta1]
+    z = A.apply_transpose(U[0])
+    alpha = _tracked_norm(c, z)
+    if alpha == 0.0:
+        return Result(x=zero, records=[], termination="trivial")
+    V = [z / alpha]
+    alphas, betas = [alpha], []
+    records = []
+    x = None
+    termination = "maxiter"
+    for k in range(1, min(maxiter, A.cols) + 1):
+        tic = time.perf_counter()
+        w = A.apply(V[-1]) - alphas[-1] * U[-1]
+        for u in U:
+            w = w - _tracked_dot(c, u, w) * u
+        beta = _tracked_norm(c, w)
+        exhausted = beta <= 1e-14 * alphas[-1]
+        if not exhausted:
+            U.append(w / beta)
+        betas.append(beta)
+        B = np.zeros((k + 1, k))
+        for j in range(k):
+            B[j, j] = alphas[j]
+            B[j + 1, j] = betas[j]
+        rhs = np.zeros(k + 1)
+        rhs[0] = beta1
+        N = np.eye(k) if lam > 0.0 else None
+        y, fallback = projected_solve(B, rhs, lam, N)
+        x = np.column_stack(V[:k]) @ y
+        if x0 is not None:
+            x = x0 + x
+        rec = _krylov_record(k, B, rhs, y, lam, N, fallback, x, x_true, A, b, diagnostics, c, tic)
+        if not exhausted:
+            z = A.apply_transpose(U[-1]) - beta * V[-1]
+            for v in V:
+                z = z - _tracked_dot(c, v, z) * v
+            alpha = _tracked_norm(c, z)
+            if alpha <= 1e-14 * beta:
+                exhausted = True
+            else:
+                V.append(z / alpha)
+                alphas.append(alpha)
+        rec["matvecs"], rec["tmatvecs"], rec["dots"], rec["sketches"] = c.snapshot()
+        records.append(rec)
+        if exhausted:
+            termination = "breakdown"
+            break
+    return Result(x=x, records=records, termination=termination)

@@ -38,7 +38,9 @@ from .solvers import (
     SolverTrace,
     TraceRecord,
     cmrh,
+    gmres,
     lslu,
+    lsqr,
     pivot_positions,
     scmrh,
     scmrh_tikhonov,

@@ -43,6 +43,7 @@ class HsConfig(ctypes.Structure):
         ("sketched", ctypes.c_int32),
         ("pivot_sample", ctypes.c_int32),
         ("pivot_positions", ctypes.c_void_p),
+        ("diagnostics", ctypes.c_int32),
     ]
 
 
@@ -79,8 +80,10 @@ _SIGNATURES = [
     ("hs_sketch_export_csr", c_i32, [c_vp, c_vp, c_vp, c_vp]),
     ("hs_sketch_destroy", c_i32, [c_vp]),
     ("hs_solve", c_i32, [c_vp, c_vp, ctypes.POINTER(HsConfig), c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.POINTER(c_vp)]),
+    ("hs_solve_krylov", c_i32, [c_vp, c_vp, ctypes.POINTER(HsConfig), c_i32, c_vp, c_vp, c_vp, ctypes.POINTER(c_vp)]),
     ("hs_result_info", c_i32, [c_vp, P_i32, P_i32, P_i32, P_i32, P_i32, P_i32]),
     ("hs_result_x", c_i32, [c_vp, c_vp]),
+    ("hs_result_resnorm", c_i32, [c_vp, c_vp]),
     ("hs_result_trace", c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     ("hs_result_pivots", c_i32, [c_vp, c_vp, c_vp]),
     ("hs_result_hessenberg", c_i32, [c_vp, c_vp, c_vp]),

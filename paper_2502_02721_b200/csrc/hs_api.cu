@@ -24,6 +24,7 @@
 #include "../../include/hessketch_b200.h"
 #include "hs_build.cuh"
 #include "hs_common.cuh"
+#include "hs_krylov.cuh"
 #include "hs_loop.cuh"
 #include "hs_ops.cuh"
 #include "hs_qr.cuh"
@@ -694,7 +695,7 @@ struct hs_result {
   bool square = true;
   long long m = 0, n = 0, ell = 0;
   int basis_dtype = HS_F64;
-  std::vector<double> x, sres, proj, relerr, wall_ms, H, W, Z, sr0, y;
+  std::vector<double> x, sres, proj, relerr, wall_ms, H, W, Z, sr0, y, resnorm;
   std::vector<int> rankfb;
   std::vector<long long> matvecs, tmatvecs, dots, sketches, t, g;
   double loop_ms = 0.0;
@@ -784,6 +785,9 @@ struct Solver {
     DBuf stb(sizeof(LoopState));
     st = stb.as<LoopState>();
     LoopState hst;
+    const bool diag = cfg.diagnostics != 0;
+    DBuf xk(diag ? n * sizeof(double) : 0), xkT(diag ? ldn * sizeof(T) : 0), axk(diag ? ldm * sizeof(T) : 0),
+        resn2(diag ? (K + 1) * sizeof(double) : 0), rpart(diag ? SMS * 2 * sizeof(double) : 0);
 
     // sampled pivoting (hessenberg.py:93-129): host-drawn positions per
     // selection slot, device copies of the permutations t / g and inverses
@@ -1106,6 +1110,20 @@ struct Solver {
         ++g_launches;
       }
       if (ovl) CK(cudaEventRecord(ev_qr, s2));
+      if (diag) {  // compute_diagnostics: x_k and |b - A x_k| (raw forward, uncounted; solvers.py:523-525)
+        if (ovl) CK(cudaStreamWaitEvent(s, ev_qr, 0));
+        xpass_kernel<B><<<grid_for(n, 256, SMS * 8), 256, (size_t)k * sizeof(double), s>>>(
+            n, L, ldn, k, Yh.as<double>() + (long long)(k - 1) * K, x0_h ? x0d.as<double>() : nullptr, nullptr,
+            xk.as<double>(), xpart.as<double>(), nullptr, st);
+        CKL();
+        convert_kernel<T, double><<<grid_for(n, 256, SMS * 8), 256, 0, s>>>(n, xk.as<double>(), xkT.as<T>());
+        CKL();
+        op->apply(xkT.p, wdt, axk.p, wdt, false);
+        resid_part_kernel<T><<<SMS * 2, 256, 0, s>>>(m, bd.as<double>(), axk.as<T>(), rpart.as<double>());
+        CKL();
+        mdot_finish_kernel<<<1, 32, 0, s>>>(SMS * 2, 1, rpart.as<double>(), resn2.as<double>() + (k - 1), 0);
+        CKL();
+      }
       if (lamon) {
         // F column k = S1 l_{k+1} (used by the projected solve of iteration k+1)
         if (ovl) {
@@ -1174,6 +1192,12 @@ struct Solver {
     CK(cudaMemcpy(res->proj.data(), projb.p, kend * sizeof(double), cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(res->rankfb.data(), rfb.p, kend * sizeof(int), cudaMemcpyDeviceToHost));
     res->relerr.assign(kend, NAN);
+    if (diag) {
+      std::vector<double> r2(kend);
+      CK(cudaMemcpy(r2.data(), resn2.p, kend * sizeof(double), cudaMemcpyDeviceToHost));
+      res->resnorm.resize(kend);
+      for (int k = 0; k < kend; ++k) res->resnorm[k] = std::sqrt(r2[k]);
+    }
     if (xt_h) {
       std::vector<double> r2(K + 1);
       CK(cudaMemcpy(r2.data(), rel2.p, (K + 1) * sizeof(double), cudaMemcpyDeviceToHost));
@@ -1310,6 +1334,7 @@ int hs_ctx_synchronize(hs_ctx* ctx) { return guarded([&] { CK(cudaStreamSynchron
 
 }  // extern "C"
 
+#include "hs_krylov.inc"
 #include "hs_dist.inc"
 
 #include "hs_abi.inc"

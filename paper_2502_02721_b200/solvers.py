@@ -20,8 +20,14 @@ Device knobs added to :class:`SolverConfig` (defaults reproduce the reference):
 * ``record_rel_err`` -- compute rel_err at every iteration (default True when
                       x_true is given, as the reference does)
 
-Out of scope in this version (raise NotImplementedError): the GMRES/LSQR
-references, ``compute_diagnostics=True``, ``printed_f_columns=True``.
+The reference's comparison solvers ``gmres`` / ``lsqr`` (solvers.py:256-403)
+also run on the device (``hs_solve_krylov``).
+
+``compute_diagnostics=True`` computes the exact residual ``res_norm`` =
+|b - A x_k| on the device every iteration (solvers.py:523-525, 247-250); the
+condition numbers / embedding distortion (``kappa_basis``, ``kappa_dbar``,
+``eps_embed``, SVDs of the full bases) stay None.  Out of scope (raises
+NotImplementedError): ``printed_f_columns=True``.
 """
 
 from __future__ import annotations
@@ -55,6 +61,8 @@ __all__ = [
     "slslu_tikhonov",
     "cmrh",
     "lslu",
+    "gmres",
+    "lsqr",
     "SOLVERS",
 ]
 
@@ -184,6 +192,9 @@ class _NativeResult:
         self.x = np.empty(cols)
         _lib.check(lib.hs_result_x(handle, _lib.ptr(self.x)))
         n = max(nrec, 1)
+        self.resnorm = np.full(n, np.nan)
+        if nrec:
+            _lib.check(lib.hs_result_resnorm(handle, _lib.ptr(self.resnorm)))
         self.sres, self.proj, self.relerr, self.wall = (np.empty(n) for _ in range(4))
         self.rankfb = np.empty(n, dtype=np.int32)
         self.matvecs, self.tmatvecs, self.dots, self.sketches = (np.empty(n, dtype=np.int64) for _ in range(4))
@@ -257,8 +268,6 @@ def _hessenberg_solve(A, b, cfg, x_true, square, sketch_basis, sketch=None, S1=N
     cfg = cfg or SolverConfig()
     if square and not A.is_square:
         raise ValueError("this solver needs a square operator")
-    if cfg.compute_diagnostics:
-        raise NotImplementedError("compute_diagnostics is out of scope for the device path")
     b = np.ascontiguousarray(b, dtype=np.float64)
     if b.shape != (A.rows,):
         raise ValueError(f"b must have length {A.rows}, got shape {b.shape}")
@@ -303,6 +312,7 @@ def _hessenberg_solve(A, b, cfg, x_true, square, sketch_basis, sketch=None, S1=N
         record_x=1 if (x_true is not None and cfg.record_rel_err) else 0, lam=float(cfg.lam),
         sketched=1 if sketched else 0, pivot_sample=0 if positions is None else int(cfg.pivot.sample_size),
         pivot_positions=None if positions is None else positions.ctypes.data,
+        diagnostics=1 if cfg.compute_diagnostics else 0,
     )
     h = _lib.c_vp()
     _lib.check(_lib.load().hs_solve(dev.ctx.handle, dev.handle, ctypes.byref(hc),
@@ -321,6 +331,7 @@ def _hessenberg_solve(A, b, cfg, x_true, square, sketch_basis, sketch=None, S1=N
             sres_norm=float(nr.sres[i]) if sketched else None,
             proj_obj=float(nr.proj[i]),
             rel_err=None if (x_true is None or np.isnan(rel)) else rel,
+            res_norm=float(nr.resnorm[i]) if cfg.compute_diagnostics else None,
             matvecs=int(nr.matvecs[i]), tmatvecs=int(nr.tmatvecs[i]), dots=int(nr.dots[i]),
             sketches=int(nr.sketches[i]), wall_ms=float(nr.wall[i]), rank_fallback=bool(nr.rankfb[i]),
         ))
@@ -351,6 +362,55 @@ def slslu_tikhonov(A, b, cfg=None, x_true=None, *, printed_f_columns=False):
     return _hessenberg_solve(A, b, cfg, x_true, False, False)
 
 
+def _krylov_solve(A, b, cfg, x_true, method):
+    """gmres / lsqr (solvers.py:256-403) on the device through ``hs_solve_krylov``."""
+    cfg = cfg or SolverConfig()
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    if b.shape != (A.rows,):
+        raise ValueError(f"b must have length {A.rows}, got shape {b.shape}")
+    x0 = None if cfg.x0 is None else np.ascontiguousarray(cfg.x0, dtype=np.float64)
+    dev = to_device_operator(A)
+    if x_true is not None:
+        x_true = np.ascontiguousarray(x_true, dtype=np.float64)
+    hc = _lib.HsConfig(maxiter=cfg.maxiter, square=1 if method == 0 else 0, sketch_basis=0,
+                       work_dtype=_lib.DTYPE_CODES[cfg.dtype], basis_dtype=_lib.DTYPE_CODES[cfg.dtype],
+                       record_x=1 if x_true is not None else 0, lam=float(cfg.lam), sketched=0, pivot_sample=0,
+                       pivot_positions=None, diagnostics=1 if cfg.compute_diagnostics else 0)
+    h = _lib.c_vp()
+    _lib.check(_lib.load().hs_solve_krylov(dev.ctx.handle, dev.handle, ctypes.byref(hc), method, _lib.ptr(b),
+                                           _lib.ptr(x0), _lib.ptr(x_true), ctypes.byref(h)))
+    nr = _NativeResult(h, A.rows, A.cols, min(cfg.maxiter, A.cols) + 1)
+    term = nr.info["termination"]
+    if term == "trivial":
+        return SolveResult(x=nr.x, trace=SolverTrace(), termination="trivial")
+    trace = SolverTrace()
+    for i in range(nr.info["n_records"]):
+        rel = float(nr.relerr[i])
+        trace.records.append(TraceRecord(
+            iteration=i + 1, proj_obj=float(nr.proj[i]),
+            rel_err=None if (x_true is None or np.isnan(rel)) else rel,
+            res_norm=float(nr.resnorm[i]) if cfg.compute_diagnostics else None,
+            matvecs=int(nr.matvecs[i]), tmatvecs=int(nr.tmatvecs[i]), dots=int(nr.dots[i]),
+            sketches=0, wall_ms=float(nr.wall[i]), rank_fallback=bool(nr.rankfb[i]),
+        ))
+    return SolveResult(x=nr.x, trace=trace, termination=term, loop_ms=nr.loop_ms)
+
+
+def gmres(A, b, cfg=None, x_true=None):
+    """Arnoldi minimal-residual reference for square systems (solvers.py:256-325):
+    Gram-Schmidt with one reorthogonalisation pass, tracked inner products,
+    lucky breakdown at h_{k+1,k} <= 1e-14 |h|, lam^2 |y|^2 damping."""
+    if not A.is_square:
+        raise ValueError("gmres needs a square operator")
+    return _krylov_solve(A, b, cfg, x_true, 0)
+
+
+def lsqr(A, b, cfg=None, x_true=None):
+    """Golub-Kahan least-squares reference (solvers.py:328-403), both sequences
+    reorthogonalised; lam > 0 gives damped least squares on the Krylov space."""
+    return _krylov_solve(A, b, cfg, x_true, 1)
+
+
 def cmrh(A, b, cfg=None, x_true=None):
     """Quasi-minimal residual on the pivoted Hessenberg basis (solvers.py:542-550):
     min |beta e1 - H_{k+1,k} y| (+ lam^2 |y|^2), x = L_k y."""
@@ -363,6 +423,8 @@ def lslu(A, b, cfg=None, x_true=None):
 
 
 SOLVERS = {
+    "gmres": gmres,
+    "lsqr": lsqr,
     "cmrh": cmrh,
     "lslu": lslu,
     "scmrh": scmrh,

@@ -46,6 +46,8 @@ def _pack_result(res, prefix=""):
     for name in ("matvecs", "tmatvecs", "dots", "sketches"):
         out[prefix + name] = np.array([getattr(r, name) for r in recs], dtype=np.int64)
     out[prefix + "rank_fallback"] = np.array([r.rank_fallback for r in recs], dtype=bool)
+    if any(r.res_norm is not None for r in recs):
+        out[prefix + "res_norm"] = np.array([np.nan if r.res_norm is None else r.res_norm for r in recs])
     st = res.factorization
     if st is not None:
         out[prefix + "H"] = st.H_matrix()
@@ -366,6 +368,46 @@ def gen_exchange():
     _save("exchange", **o)
 
 
+def gen_krylov():
+    """The comparison solvers gmres / lsqr (solvers.py:256-403), with
+    diagnostics (res_norm), damping, x0, lucky breakdown and exhaustion."""
+    o = {}
+    rng = np.random.default_rng(505)
+    n = 40
+    M = rng.standard_normal((n, n)) + 4.0 * np.eye(n)
+    b = rng.standard_normal(n)
+    xt = np.linalg.solve(M, b)
+    A = LinearOperator.from_matrix(M)
+    o.update(sq_M=M, sq_b=b, sq_x_true=xt)
+    diag = solvers.SolverConfig(maxiter=15, compute_diagnostics=True)
+    o.update(_pack_result(solvers.gmres(A, b, diag, x_true=xt), "gm_"))
+    o.update(_pack_result(solvers.gmres(A, b, solvers.SolverConfig(maxiter=12, lam=0.3), x_true=xt), "gm_tik_"))
+    x0 = rng.standard_normal(n) * 0.1
+    o["x0"] = x0
+    o.update(_pack_result(solvers.gmres(A, b, solvers.SolverConfig(maxiter=8, x0=x0, compute_diagnostics=True)), "gm_x0_"))
+    o.update(_pack_result(solvers.gmres(LinearOperator.identity(3), np.array([3.0, -5.0, 2.0])), "gm_id_"))
+    rng = np.random.default_rng(606)
+    m, nn = 60, 25
+    Mr = rng.standard_normal((m, nn))
+    br = rng.standard_normal(m)
+    xr = np.linalg.lstsq(Mr, br, rcond=None)[0]
+    Ar = LinearOperator.from_matrix(Mr)
+    o.update(re_M=Mr, re_b=br, re_x_true=xr)
+    o.update(_pack_result(solvers.lsqr(Ar, br, solvers.SolverConfig(maxiter=15, compute_diagnostics=True), x_true=xr), "ls_"))
+    o.update(_pack_result(solvers.lsqr(Ar, br, solvers.SolverConfig(maxiter=10, lam=0.5), x_true=xr), "ls_tik_"))
+    x0r = rng.standard_normal(nn) * 0.1
+    o["x0r"] = x0r
+    o.update(_pack_result(solvers.lsqr(Ar, br, solvers.SolverConfig(maxiter=8, x0=x0r)), "ls_x0_"))
+    Mw = rng.standard_normal((8, 3))
+    bw = rng.standard_normal(8)
+    o.update(w_M=Mw, w_b=bw)
+    o.update(_pack_result(solvers.lsqr(LinearOperator.from_matrix(Mw), bw, solvers.SolverConfig(maxiter=6)), "ls_w_"))
+    prob = problems.make_tomography(16, 12, noise_level=0.01, seed=4)
+    o.update(_pack_result(solvers.lsqr(prob.operator, prob.b, solvers.SolverConfig(maxiter=30, compute_diagnostics=True),
+                                       x_true=prob.x_true), "ls_tomo_"))
+    _save("krylov", **o)
+
+
 if __name__ == "__main__":
     print("reference hessketch", hessketch.__version__)
     gen_pivot_and_steps()
@@ -376,3 +418,4 @@ if __name__ == "__main__":
     gen_edge()
     gen_sampled_and_unsketched()
     gen_exchange()
+    gen_krylov()

@@ -333,6 +333,87 @@ def test_sampled_pivoting_and_unsketched_vs_reference(hs, golden):
     assert hs.SOLVERS["cmrh"] is hs.cmrh and hs.SOLVERS["lslu"] is hs.lslu
 
 
+def _check_krylov(res, g, prefix, rtol=1e-9):
+    assert res.termination == str(g[prefix + "termination"])
+    recs = res.trace.records
+    assert len(recs) == len(g[prefix + "proj_obj"])
+    for name in ("matvecs", "tmatvecs", "dots", "sketches"):
+        assert [getattr(r, name) for r in recs] == list(g[prefix + name]), name
+    scale = max(1.0, float(np.max(np.abs(g[prefix + "proj_obj"]))))
+    np.testing.assert_allclose([r.proj_obj for r in recs], g[prefix + "proj_obj"], rtol=rtol, atol=1e-13 * scale)
+    if not np.all(np.isnan(g[prefix + "rel_err"])):
+        np.testing.assert_allclose([r.rel_err for r in recs], g[prefix + "rel_err"], rtol=rtol)
+    if prefix + "res_norm" in g:
+        np.testing.assert_allclose([r.res_norm for r in recs], g[prefix + "res_norm"], rtol=rtol, atol=1e-13 * scale)
+    assert all(r.sres_norm is None for r in recs)
+    assert _rel(res.x, g[prefix + "x"]) <= rtol
+
+
+def test_gmres_lsqr_vs_reference(hs, golden):
+    """gmres / lsqr on the device (classical Gram-Schmidt x2 where the reference
+    runs modified Gram-Schmidt): counters exact, x / proj_obj / rel_err /
+    res_norm within 1e-9 relative."""
+    g = golden("krylov")
+    A = hs.LinearOperator.from_matrix(g["sq_M"])
+    b, xt = g["sq_b"], g["sq_x_true"]
+    _check_krylov(hs.gmres(A, b, hs.SolverConfig(maxiter=15, compute_diagnostics=True), x_true=xt), g, "gm_")
+    _check_krylov(hs.gmres(A, b, hs.SolverConfig(maxiter=12, lam=0.3), x_true=xt), g, "gm_tik_")
+    _check_krylov(hs.gmres(A, b, hs.SolverConfig(maxiter=8, x0=g["x0"], compute_diagnostics=True)), g, "gm_x0_")
+    _check_krylov(hs.gmres(hs.LinearOperator.identity(3), np.array([3.0, -5.0, 2.0])), g, "gm_id_")
+    Ar = hs.LinearOperator.from_matrix(g["re_M"])
+    b, xt = g["re_b"], g["re_x_true"]
+    _check_krylov(hs.lsqr(Ar, b, hs.SolverConfig(maxiter=15, compute_diagnostics=True), x_true=xt), g, "ls_")
+    _check_krylov(hs.lsqr(Ar, b, hs.SolverConfig(maxiter=10, lam=0.5), x_true=xt), g, "ls_tik_")
+    _check_krylov(hs.lsqr(Ar, b, hs.SolverConfig(maxiter=8, x0=g["x0r"])), g, "ls_x0_")
+    _check_krylov(hs.lsqr(hs.LinearOperator.from_matrix(g["w_M"]), g["w_b"], hs.SolverConfig(maxiter=6)), g, "ls_w_")
+    # tomography LSQR: one-pass MGS on an ill-conditioned operator is sensitive
+    # to the dot summation order -- the reference itself moves by 3e-3 in
+    # proj_obj at k = 30 when only np.dot's order changes (oracle experiment),
+    # so: first 15 iterations at 1e-8, the rest inside that envelope
+    t = golden("slslu_tomo16")
+    K = _csr(golden("tomo_matrices"), "tomo16x12_")
+    res = hs.lsqr(hs.LinearOperator.from_matrix(K), t["b"], hs.SolverConfig(maxiter=30, compute_diagnostics=True),
+                  x_true=t["x_true"])
+    recs = res.trace.records
+    assert [r.dots for r in recs] == list(g["ls_tomo_dots"])
+    for name, rt in (("proj_obj", 1e-8), ("rel_err", 1e-8), ("res_norm", 1e-8)):
+        got = np.array([getattr(r, name) for r in recs])
+        np.testing.assert_allclose(got[:15], g["ls_tomo_" + name][:15], rtol=rt)
+        np.testing.assert_allclose(got, g["ls_tomo_" + name], rtol=6e-3)
+    with pytest.raises(ValueError):
+        hs.gmres(hs.LinearOperator.from_matrix(g["re_M"]), b)
+
+
+def test_diagnostics_res_norm_hessenberg(hs, golden):
+    """compute_diagnostics on the Hessenberg solvers: res_norm = |b - A x_k|
+    every iteration, against the oracle's restatement (x within 1e-10)."""
+    g = golden("slslu_tomo16")
+    K = _csr(g)
+    S2 = _csr(g, "S2_")
+    sk = hs.SketchOperator(S2.shape[0], S2.shape[1], 9, S2)
+    res = hs.slslu(hs.LinearOperator.from_matrix(K), g["b"], hs.SolverConfig(maxiter=20, compute_diagnostics=True),
+                   sketch=sk)
+    want = [np.linalg.norm(g["b"] - K @ x) for x in _iterates(hs, K, g["b"], S2, 20)]
+    np.testing.assert_allclose([r.res_norm for r in res.trace.records], want, rtol=1e-9)
+    gs = golden("sampled_unsketched")
+    A = hs.LinearOperator.from_matrix(gs["sq_M"])
+    res = hs.cmrh(A, gs["sq_b"], hs.SolverConfig(maxiter=10, compute_diagnostics=True))
+    r = [rec.res_norm for rec in res.trace.records]
+    Ao = ho.dense_operator(gs["sq_M"], sequential=False)
+    want = [np.linalg.norm(gs["sq_b"] - gs["sq_M"] @ ho.hessenberg_solve(Ao, gs["sq_b"], square=True, maxiter=k,
+                                                                          sketched=False).x) for k in range(1, 11)]
+    np.testing.assert_allclose(r, want, rtol=1e-9)
+    np.testing.assert_allclose(r[-1], np.linalg.norm(gs["sq_b"] - gs["sq_M"] @ res.x), rtol=1e-9)
+
+
+def _iterates(hs, K, b, S2, K_iter):
+    out = []
+    for k in range(1, K_iter + 1):
+        r = ho.hessenberg_solve(ho.csr_operator(K), b, square=False, maxiter=k, S2=S2)
+        out.append(r.x)
+    return out
+
+
 def test_python_callables_rejected(hs):
     A = hs.LinearOperator(4, 4, lambda x: x, lambda y: y)
     with pytest.raises(TypeError):
@@ -362,7 +443,9 @@ def test_validation_errors(hs):
     with pytest.raises(ValueError):
         hs.slslu(A, np.ones(7), hs.SolverConfig(maxiter=2))
     with pytest.raises(NotImplementedError):
-        hs.scmrh(A, np.ones(8), hs.SolverConfig(maxiter=2, compute_diagnostics=True))
+        hs.slslu_tikhonov(A, np.ones(8), hs.SolverConfig(maxiter=2, lam=0.1), printed_f_columns=True)
+    r = hs.scmrh(A, np.ones(8), hs.SolverConfig(maxiter=2, compute_diagnostics=True))
+    assert all(rec.res_norm is not None and rec.kappa_basis is None for rec in r.trace.records)
 
 
 def test_deterministic_replay(hs):

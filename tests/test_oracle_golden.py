@@ -254,3 +254,37 @@ def test_sampled_pivoting_and_unsketched_bitwise(golden):
     _check_result(res, g, "tomo_samp_")
     res = ho.hessenberg_solve(At, g["tomo_b"], square=False, maxiter=30, x_true=g["tomo_x_true"], sketched=False)
     _check_result(res, g, "tomo_lslu_")
+
+
+def _check_krylov(res, g, prefix):
+    assert res.termination == str(g[prefix + "termination"])
+    assert len(res.records) == len(g[prefix + "proj_obj"])
+    for name in ("matvecs", "tmatvecs", "dots", "sketches"):
+        assert [r[name] for r in res.records] == list(g[prefix + name]), name
+    for name in ("proj_obj", "rel_err"):
+        got = np.array([np.nan if r[name] is None else r[name] for r in res.records])
+        np.testing.assert_array_equal(got, g[prefix + name], err_msg=name)
+    if prefix + "res_norm" in g:
+        np.testing.assert_array_equal([r["res_norm"] for r in res.records], g[prefix + "res_norm"])
+    np.testing.assert_array_equal(res.x, g[prefix + "x"])
+
+
+def test_gmres_lsqr_bitwise(golden):
+    """The comparison solvers restated (solvers.py:256-403): counters including
+    the tracked inner products, x, proj_obj, rel_err, res_norm bit for bit."""
+    g = golden("krylov")
+    A = ho.dense_operator(g["sq_M"], sequential=False)
+    b, xt = g["sq_b"], g["sq_x_true"]
+    _check_krylov(ho.gmres(A, b, maxiter=15, x_true=xt, diagnostics=True), g, "gm_")
+    _check_krylov(ho.gmres(A, b, maxiter=12, lam=0.3, x_true=xt), g, "gm_tik_")
+    _check_krylov(ho.gmres(A, b, maxiter=8, x0=g["x0"], diagnostics=True), g, "gm_x0_")
+    _check_krylov(ho.gmres(ho.identity_operator(3), np.array([3.0, -5.0, 2.0]), maxiter=30), g, "gm_id_")
+    Ar = ho.dense_operator(g["re_M"], sequential=False)
+    b, xt = g["re_b"], g["re_x_true"]
+    _check_krylov(ho.lsqr(Ar, b, maxiter=15, x_true=xt, diagnostics=True), g, "ls_")
+    _check_krylov(ho.lsqr(Ar, b, maxiter=10, lam=0.5, x_true=xt), g, "ls_tik_")
+    _check_krylov(ho.lsqr(Ar, b, maxiter=8, x0=g["x0r"]), g, "ls_x0_")
+    _check_krylov(ho.lsqr(ho.dense_operator(g["w_M"], sequential=False), g["w_b"], maxiter=6), g, "ls_w_")
+    t = golden("slslu_tomo16")
+    K = _csr(golden("tomo_matrices"), "tomo16x12_")
+    _check_krylov(ho.lsqr(ho.csr_operator(K), t["b"], maxiter=30, x_true=t["x_true"], diagnostics=True), g, "ls_tomo_")
