@@ -83,8 +83,10 @@ typedef struct {
      draw.  Positions index the swap-ordered admissible list t[k:] / g[k:]
      (hessenberg.py:127-129), which the device maintains.                   */
   const int64_t* pivot_positions;
-  int32_t diagnostics;   /* compute_diagnostics: exact residual |b - A x_k| per
-                            iteration (solvers.py:523-525), hs_result_resnorm  */
+  int32_t diagnostics;   /* compute_diagnostics (solvers.py:523-532): exact
+                            residual |b - A x_k| (hs_result_resnorm); Hessenberg
+                            solvers also kappa_basis, kappa_dbar, eps_embed
+                            (hs_result_diagnostics); serialises the loop      */
 } hs_config;
 
 const char* hs_last_error(void);
@@ -163,6 +165,9 @@ int hs_result_info(const hs_result* r, int32_t* n_records, int32_t* termination,
 int hs_result_x(const hs_result* r, double* x);                 /* n */
 /* per record |b - A x_k| when cfg->diagnostics was set, else NaN */
 int hs_result_resnorm(const hs_result* r, double* out);
+/* per record kappa_basis, kappa_dbar (lam > 0), eps_embed (sketched, column
+   sketching) when cfg->diagnostics was set (Hessenberg solvers), else NaN */
+int hs_result_diagnostics(const hs_result* r, double* kappa_basis, double* kappa_dbar, double* eps_embed);
 /* per record: sres_norm, proj_obj, rel_err (NaN if no x_true), rank_fallback,
    counters (matvecs, tmatvecs, dots, sketches), wall_ms (device events) */
 int hs_result_trace(const hs_result* r, double* sres, double* proj, double* relerr, int32_t* rank_fallback,

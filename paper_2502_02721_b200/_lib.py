@@ -84,6 +84,7 @@ _SIGNATURES = [
     ("hs_result_info", c_i32, [c_vp, P_i32, P_i32, P_i32, P_i32, P_i32, P_i32]),
     ("hs_result_x", c_i32, [c_vp, c_vp]),
     ("hs_result_resnorm", c_i32, [c_vp, c_vp]),
+    ("hs_result_diagnostics", c_i32, [c_vp, c_vp, c_vp, c_vp]),
     ("hs_result_trace", c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     ("hs_result_pivots", c_i32, [c_vp, c_vp, c_vp]),
     ("hs_result_hessenberg", c_i32, [c_vp, c_vp, c_vp]),

@@ -24,6 +24,7 @@
 #include "../../include/hessketch_b200.h"
 #include "hs_build.cuh"
 #include "hs_common.cuh"
+#include "hs_diag.cuh"
 #include "hs_krylov.cuh"
 #include "hs_loop.cuh"
 #include "hs_ops.cuh"
@@ -695,7 +696,7 @@ struct hs_result {
   bool square = true;
   long long m = 0, n = 0, ell = 0;
   int basis_dtype = HS_F64;
-  std::vector<double> x, sres, proj, relerr, wall_ms, H, W, Z, sr0, y, resnorm;
+  std::vector<double> x, sres, proj, relerr, wall_ms, H, W, Z, sr0, y, resnorm, kappa_basis, kappa_dbar, eps_embed;
   std::vector<int> rankfb;
   std::vector<long long> matvecs, tmatvecs, dots, sketches, t, g;
   double loop_ms = 0.0;
@@ -712,6 +713,73 @@ struct hs_result {
 // the solver
 
 namespace {
+
+// Incremental QR (classical Gram-Schmidt, one reorthogonalisation) of a
+// growing set of device columns, for the condition-number diagnostics
+// (hs_diag.cuh).  Q and R in fp64.
+struct DiagQR {
+  hs_ctx* ctx = nullptr;
+  long long len = 0, ld = 0;
+  int cap = 0, cnt = 0;
+  DBuf Q, R, v, rtmp, part, sq;
+  void init(hs_ctx* c, long long n, int capacity) {
+    ctx = c;
+    len = n;
+    ld = (n + 63) / 64 * 64;
+    cap = capacity;
+    cnt = 0;
+    Q.alloc((size_t)cap * ld * sizeof(double));
+    R.alloc((size_t)cap * cap * sizeof(double));
+    v.alloc(ld * sizeof(double));
+    rtmp.alloc((cap + 1) * sizeof(double));
+    part.alloc((size_t)c->num_sms * 2 * (cap + 1) * sizeof(double));
+    sq.alloc(2 * sizeof(double));
+  }
+  template <class X>
+  void append(const X* col) {
+    if (cnt >= cap) fail(HS_ERR_RUNTIME, "diagnostic QR capacity exceeded");
+    cudaStream_t s = ctx->stream;
+    const int NB = ctx->num_sms * 2, G = ctx->num_sms * 8;
+    double* vq = v.as<double>();
+    to_f64_kernel<X><<<grid_for(len, 256, G), 256, 0, s>>>(len, col, vq);
+    CKL();
+    double* rc = R.as<double>() + (long long)cnt * cap;
+    const double* Qp = Q.as<double>();
+    for (int pass = 0; pass < 2 && cnt > 0; ++pass) {
+      double* coef = pass == 0 ? rc : rtmp.as<double>();
+      mdot_kernel<double><<<NB, 256, 0, s>>>(len, Qp, ld, cnt, vq, part.as<double>());
+      CKL();
+      mdot_finish_kernel<<<(cnt + 127) / 128, 128, 0, s>>>(NB, cnt, part.as<double>(), coef, 0);
+      CKL();
+      maxpy_kernel<double><<<grid_for(len, 256, G), 256, (size_t)cnt * sizeof(double), s>>>(len, Qp, ld, cnt, coef, vq);
+      CKL();
+      if (pass == 1) {
+        add_into_kernel<<<(cnt + 127) / 128, 128, 0, s>>>(cnt, rc, rtmp.as<double>());
+        CKL();
+      }
+    }
+    mdot_kernel<double><<<NB, 256, 0, s>>>(len, vq, 0, 1, vq, part.as<double>());
+    CKL();
+    mdot_finish_kernel<<<1, 32, 0, s>>>(NB, 1, part.as<double>(), sq.as<double>(), 0);
+    CKL();
+    qr_col_finish_kernel<<<1, 1, 0, s>>>(cnt, sq.as<double>(), rc, sq.as<double>() + 1);
+    CKL();
+    double* qn = Q.as<double>() + (long long)cnt * ld;
+    CK(cudaMemcpyAsync(qn, vq, len * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    scale_inv_kernel<<<grid_for(len, 256, G), 256, 0, s>>>(len, qn, sq.as<double>() + 1);
+    CKL();
+    ++cnt;
+  }
+  // singular values of the leading kk columns (R[:kk, :kk]) into sv
+  void singular_values(int kk, double* sv, DBuf& work) {
+    cudaStream_t s = ctx->stream;
+    if (work.bytes < (size_t)kk * kk * sizeof(double)) work.alloc((size_t)cap * cap * sizeof(double));
+    r_block_kernel<<<(kk * kk + 255) / 256, 256, 0, s>>>(kk, R.as<double>(), cap, work.as<double>());
+    CKL();
+    jacobi_sv_kernel<<<1, 1024, 0, s>>>(kk, kk, work.as<double>(), kk, sv, 40);
+    CKL();
+  }
+};
 
 template <class T, class B>
 struct Solver {
@@ -788,6 +856,24 @@ struct Solver {
     const bool diag = cfg.diagnostics != 0;
     DBuf xk(diag ? n * sizeof(double) : 0), xkT(diag ? ldn * sizeof(T) : 0), axk(diag ? ldm * sizeof(T) : 0),
         resn2(diag ? (K + 1) * sizeof(double) : 0), rpart(diag ? SMS * 2 * sizeof(double) : 0);
+    // condition numbers / embedding distortion (solvers.py:526-532): incremental
+    // QR of the data basis (qB, rectangular), the solution basis (qL) and
+    // [r0, A l_1, ...] (qW); Jacobi SVDs of the small factors (hs_diag.cuh)
+    DiagQR qB, qL, qW;
+    DBuf svA, svB, djac, Xw, Mw, kbuf;
+    const bool diag_eps = diag && skd && !sb;
+    if (diag) {
+      qL.init(ctx, n, K + 2);
+      if (!square) qB.init(ctx, m, K + 2);
+      if (diag_eps) {
+        qW.init(ctx, m, K + 2);
+        Xw.alloc((size_t)ell * (K + 2) * sizeof(double));
+        Mw.alloc((size_t)ell * (K + 2) * sizeof(double));
+      }
+      svA.alloc((K + 2) * sizeof(double));
+      svB.alloc((K + 2) * sizeof(double));
+      kbuf.alloc((size_t)3 * (K + 1) * sizeof(double));
+    }
 
     // sampled pivoting (hessenberg.py:93-129): host-drawn positions per
     // selection slot, device copies of the permutations t / g and inverses
@@ -966,6 +1052,15 @@ struct Solver {
     }
     (void)first_basis;
 
+    if (diag) {
+      if (square) {
+        qL.append(Lcol(0));
+      } else {
+        qB.append(Dcol(0));
+        qL.append(Lcol(0));
+      }
+      if (diag_eps) qW.append(r0.as<T>());
+    }
     if (timing) CK(cudaStreamSynchronize(s));
     const auto t_init = now();
     // ---- the loop (solvers.py:468-538)
@@ -1005,7 +1100,7 @@ struct Solver {
     // basis work; u is not overwritten by the elimination (it writes u2), the
     // next A-apply waits for the sketch to have read u, and the fused iterate
     // of iteration k+1 waits for y^{(k)}.
-    const bool ovl = skd && !sb && !env_flag("HS_NO_OVERLAP");  // knob: serialise for A/B
+    const bool ovl = skd && !sb && !diag && !env_flag("HS_NO_OVERLAP");  // knob: serialise for A/B
     cudaStream_t s2 = ovl ? ctx->aux : s;
     DBuf u2(ovl ? ldm * sizeof(T) : 0);
     T* uel = ovl ? u2.as<T>() : u.as<T>();  // elimination output on the side that is sketched
@@ -1042,11 +1137,14 @@ struct Solver {
       // u is free once the previous iteration's sketch has read it
       if (ovl && k > 1) CK(cudaStreamWaitEvent(s, ev_sk, 0));
       op->apply(Lcol(k - 1), bdt, u.p, wdt, false);
+      if (diag_eps) qW.append(u.as<T>());  // the unreduced A l_k (solvers.py:480-481)
       if (ovl) {
         CK(cudaEventRecord(ev_u, s));
         CK(cudaStreamWaitEvent(s2, ev_u, 0));
         S2->apply(u.p, wdt, Zb.as<double>() + (long long)(k - 1) * ell, s2);
         CK(cudaEventRecord(ev_sk, s2));
+      } else if (skd && !sb && !square) {  // serialised (diagnostics): sketch before the in-place elimination
+        S2->apply(u.p, wdt, Zb.as<double>() + (long long)(k - 1) * ell);
       }
       // the fused iterate x_{k-1} needs y^{(k-1)} from the aux stream
       auto wait_y = [&] {
@@ -1123,6 +1221,37 @@ struct Solver {
         CKL();
         mdot_finish_kernel<<<1, 32, 0, s>>>(SMS * 2, 1, rpart.as<double>(), resn2.as<double>() + (k - 1), 0);
         CKL();
+        // which bases grew this iteration (hessenberg.py:219-224, 356-389)
+        CK(cudaMemcpyAsync(&hst, st, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const bool bd_now = hst.bd_iter == k;
+        if (square) {
+          if (!bd_now) qL.append(Lcol(k));
+        } else {
+          if (!(bd_now && hst.bd_side == 0)) qB.append(Dcol(k));
+          if (!bd_now) qL.append(Lcol(k));
+        }
+        DiagQR& qb = square ? qL : qB;
+        double* kb = kbuf.as<double>();
+        qb.singular_values(qb.cnt, svA.as<double>(), djac);
+        kappa_kernel<<<1, 1, 0, s>>>(qb.cnt, svA.as<double>(), 0, nullptr, 0, kb + (k - 1));
+        CKL();
+        if (lamon) {  // kappa_dbar = cond of [basis, L_k] (union of singular values)
+          qL.singular_values(k, svB.as<double>(), djac);
+          kappa_kernel<<<1, 1, 0, s>>>(qb.cnt, svA.as<double>(), k, svB.as<double>(), 0, kb + (K + 1) + (k - 1));
+          CKL();
+        }
+        if (diag_eps) {  // eps of S2 on span[r0, A l_1..A l_k]: S Q = [S r0, Z] R_W^{-1}
+          CK(cudaMemcpyAsync(Xw.p, sr0.p, ell * sizeof(double), cudaMemcpyDeviceToDevice, s));
+          CK(cudaMemcpyAsync(Xw.as<double>() + ell, Zb.p, (size_t)ell * k * sizeof(double), cudaMemcpyDeviceToDevice, s));
+          trsm_right_kernel<<<(int)((ell + 127) / 128), 128, 0, s>>>((int)ell, k + 1, Xw.as<double>(), (int)ell,
+                                                                     qW.R.as<double>(), qW.cap, Mw.as<double>());
+          CKL();
+          jacobi_sv_kernel<<<1, 1024, 0, s>>>((int)ell, k + 1, Mw.as<double>(), (int)ell, svB.as<double>(), 40);
+          CKL();
+          kappa_kernel<<<1, 1, 0, s>>>(k + 1, svB.as<double>(), 0, nullptr, 1, kb + 2 * (K + 1) + (k - 1));
+          CKL();
+        }
       }
       if (lamon) {
         // F column k = S1 l_{k+1} (used by the projected solve of iteration k+1)
@@ -1197,6 +1326,13 @@ struct Solver {
       CK(cudaMemcpy(r2.data(), resn2.p, kend * sizeof(double), cudaMemcpyDeviceToHost));
       res->resnorm.resize(kend);
       for (int k = 0; k < kend; ++k) res->resnorm[k] = std::sqrt(r2[k]);
+      std::vector<double> kb((size_t)3 * (K + 1));
+      CK(cudaMemcpy(kb.data(), kbuf.p, kb.size() * sizeof(double), cudaMemcpyDeviceToHost));
+      res->kappa_basis.assign(kb.begin(), kb.begin() + kend);
+      res->kappa_dbar.assign(kend, NAN);
+      res->eps_embed.assign(kend, NAN);
+      if (lamon) std::copy(kb.begin() + (K + 1), kb.begin() + (K + 1) + kend, res->kappa_dbar.begin());
+      if (diag_eps) std::copy(kb.begin() + 2 * (K + 1), kb.begin() + 2 * (K + 1) + kend, res->eps_embed.begin());
     }
     if (xt_h) {
       std::vector<double> r2(K + 1);

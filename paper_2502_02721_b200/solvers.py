@@ -23,11 +23,14 @@ Device knobs added to :class:`SolverConfig` (defaults reproduce the reference):
 The reference's comparison solvers ``gmres`` / ``lsqr`` (solvers.py:256-403)
 also run on the device (``hs_solve_krylov``).
 
-``compute_diagnostics=True`` computes the exact residual ``res_norm`` =
-|b - A x_k| on the device every iteration (solvers.py:523-525, 247-250); the
-condition numbers / embedding distortion (``kappa_basis``, ``kappa_dbar``,
-``eps_embed``, SVDs of the full bases) stay None.  Out of scope (raises
-NotImplementedError): ``printed_f_columns=True``.
+``compute_diagnostics=True`` computes, on the device, every iteration: the
+exact residual ``res_norm`` = |b - A x_k| (solvers.py:247-250, 523-525), the
+basis condition number ``kappa_basis`` and, with lam > 0, ``kappa_dbar``
+(``_union_condition``, solvers.py:228-233, 526-530; incremental QR of the
+bases + Jacobi SVD of the small R factors), and the measured embedding
+distortion ``eps_embed`` of S2 on span[A l_1..A l_k, r0] (sketch.py:91-112;
+not for ``sketch_basis=True``).  The loop is serialised while diagnostics are
+on.  Out of scope (raises NotImplementedError): ``printed_f_columns=True``.
 """
 
 from __future__ import annotations
@@ -193,8 +196,11 @@ class _NativeResult:
         _lib.check(lib.hs_result_x(handle, _lib.ptr(self.x)))
         n = max(nrec, 1)
         self.resnorm = np.full(n, np.nan)
+        self.kappa_basis, self.kappa_dbar, self.eps_embed = (np.full(n, np.nan) for _ in range(3))
         if nrec:
             _lib.check(lib.hs_result_resnorm(handle, _lib.ptr(self.resnorm)))
+            _lib.check(lib.hs_result_diagnostics(handle, _lib.ptr(self.kappa_basis), _lib.ptr(self.kappa_dbar),
+                                                 _lib.ptr(self.eps_embed)))
         self.sres, self.proj, self.relerr, self.wall = (np.empty(n) for _ in range(4))
         self.rankfb = np.empty(n, dtype=np.int32)
         self.matvecs, self.tmatvecs, self.dots, self.sketches = (np.empty(n, dtype=np.int64) for _ in range(4))
@@ -231,6 +237,12 @@ class _NativeResult:
             except Exception:
                 pass
             self.handle = None
+
+
+def _opt(v):
+    """NaN (not computed) -> None, as the reference's optional trace fields."""
+    v = float(v)
+    return None if np.isnan(v) else v
 
 
 def _default_sketch(cfg, ell, in_rows, seed):
@@ -332,6 +344,9 @@ def _hessenberg_solve(A, b, cfg, x_true, square, sketch_basis, sketch=None, S1=N
             proj_obj=float(nr.proj[i]),
             rel_err=None if (x_true is None or np.isnan(rel)) else rel,
             res_norm=float(nr.resnorm[i]) if cfg.compute_diagnostics else None,
+            kappa_basis=_opt(nr.kappa_basis[i]) if cfg.compute_diagnostics else None,
+            kappa_dbar=_opt(nr.kappa_dbar[i]) if cfg.compute_diagnostics else None,
+            eps_embed=_opt(nr.eps_embed[i]) if cfg.compute_diagnostics else None,
             matvecs=int(nr.matvecs[i]), tmatvecs=int(nr.tmatvecs[i]), dots=int(nr.dots[i]),
             sketches=int(nr.sketches[i]), wall_ms=float(nr.wall[i]), rank_fallback=bool(nr.rankfb[i]),
         ))
@@ -390,6 +405,7 @@ def _krylov_solve(A, b, cfg, x_true, method):
             iteration=i + 1, proj_obj=float(nr.proj[i]),
             rel_err=None if (x_true is None or np.isnan(rel)) else rel,
             res_norm=float(nr.resnorm[i]) if cfg.compute_diagnostics else None,
+            kappa_basis=_opt(nr.kappa_basis[i]) if cfg.compute_diagnostics else None,
             matvecs=int(nr.matvecs[i]), tmatvecs=int(nr.tmatvecs[i]), dots=int(nr.dots[i]),
             sketches=0, wall_ms=float(nr.wall[i]), rank_fallback=bool(nr.rankfb[i]),
         ))

@@ -46,8 +46,9 @@ def _pack_result(res, prefix=""):
     for name in ("matvecs", "tmatvecs", "dots", "sketches"):
         out[prefix + name] = np.array([getattr(r, name) for r in recs], dtype=np.int64)
     out[prefix + "rank_fallback"] = np.array([r.rank_fallback for r in recs], dtype=bool)
-    if any(r.res_norm is not None for r in recs):
-        out[prefix + "res_norm"] = np.array([np.nan if r.res_norm is None else r.res_norm for r in recs])
+    for name in ("res_norm", "kappa_basis", "kappa_dbar", "eps_embed"):
+        if any(getattr(r, name) is not None for r in recs):
+            out[prefix + name] = np.array([np.nan if getattr(r, name) is None else getattr(r, name) for r in recs])
     st = res.factorization
     if st is not None:
         out[prefix + "H"] = st.H_matrix()
@@ -408,6 +409,36 @@ def gen_krylov():
     _save("krylov", **o)
 
 
+def gen_diagnostics():
+    """compute_diagnostics on the Hessenberg solvers (solvers.py:523-532):
+    res_norm, kappa_basis, kappa_dbar (lam > 0), eps_embed."""
+    o = {}
+    rng = np.random.default_rng(707)
+    n = 30
+    M = rng.standard_normal((n, n)) + 4.0 * np.eye(n)
+    b = rng.standard_normal(n)
+    A = LinearOperator.from_matrix(M)
+    o.update(sq_M=M, sq_b=b)
+    o["sq_S2"] = make_gaussian_sketch(130, n, 3).entries
+    o.update(_pack_result(solvers.scmrh(A, b, solvers.SolverConfig(maxiter=12, seed=3, compute_diagnostics=True)), "sc_"))
+    o["sqt_S2"] = make_gaussian_sketch(130, n, 4).entries
+    o["sqt_S1"] = make_gaussian_sketch(130, n, derive_seed(4, 1)).entries
+    o.update(_pack_result(solvers.scmrh_tikhonov(A, b, solvers.SolverConfig(maxiter=10, seed=4, lam=0.2,
+                                                                             compute_diagnostics=True)), "sct_"))
+    o.update(_pack_result(solvers.cmrh(A, b, solvers.SolverConfig(maxiter=12, compute_diagnostics=True)), "cm_"))
+    m, nn = 50, 20
+    Mr = rng.standard_normal((m, nn))
+    br = rng.standard_normal(m)
+    Ar = LinearOperator.from_matrix(Mr)
+    o.update(re_M=Mr, re_b=br)
+    o["re_S2"] = make_gaussian_sketch(120, m, 5).entries
+    o["re_S1"] = make_gaussian_sketch(120, nn, derive_seed(5, 1)).entries
+    o.update(_pack_result(solvers.slslu_tikhonov(Ar, br, solvers.SolverConfig(maxiter=11, seed=5, lam=0.3,
+                                                                               compute_diagnostics=True)), "sl_"))
+    o.update(_pack_result(solvers.lslu(Ar, br, solvers.SolverConfig(maxiter=11, compute_diagnostics=True)), "ll_"))
+    _save("diagnostics", **o)
+
+
 if __name__ == "__main__":
     print("reference hessketch", hessketch.__version__)
     gen_pivot_and_steps()
@@ -419,3 +450,4 @@ if __name__ == "__main__":
     gen_sampled_and_unsketched()
     gen_exchange()
     gen_krylov()
+    gen_diagnostics()

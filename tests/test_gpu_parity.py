@@ -406,6 +406,39 @@ def test_diagnostics_res_norm_hessenberg(hs, golden):
     np.testing.assert_allclose(r[-1], np.linalg.norm(gs["sq_b"] - gs["sq_M"] @ res.x), rtol=1e-9)
 
 
+def test_diagnostics_condition_numbers_vs_reference(hs, golden):
+    """compute_diagnostics: kappa_basis, kappa_dbar (lam > 0), eps_embed and
+    res_norm against the reference (SVDs of the full bases there; incremental
+    QR + Jacobi SVD of the small factors here): within 1e-8 relative."""
+    g = golden("diagnostics")
+    A = hs.LinearOperator.from_matrix(g["sq_M"])
+    Ar = hs.LinearOperator.from_matrix(g["re_M"])
+    S = lambda M: hs.SketchOperator(M.shape[0], M.shape[1], 0, M)
+    cases = [
+        ("sc_", lambda: hs.scmrh(A, g["sq_b"], hs.SolverConfig(maxiter=12, seed=3, compute_diagnostics=True))),
+        ("sct_", lambda: hs.scmrh_tikhonov(A, g["sq_b"], hs.SolverConfig(maxiter=10, seed=4, lam=0.2,
+                                                                         compute_diagnostics=True))),
+        ("cm_", lambda: hs.cmrh(A, g["sq_b"], hs.SolverConfig(maxiter=12, compute_diagnostics=True))),
+        ("sl_", lambda: hs.slslu_tikhonov(Ar, g["re_b"], hs.SolverConfig(maxiter=11, seed=5, lam=0.3,
+                                                                         compute_diagnostics=True))),
+        ("ll_", lambda: hs.lslu(Ar, g["re_b"], hs.SolverConfig(maxiter=11, compute_diagnostics=True))),
+    ]
+    for prefix, fn in cases:
+        recs = fn().trace.records
+        assert len(recs) == len(g[prefix + "proj_obj"]), prefix
+        for name in ("res_norm", "kappa_basis", "kappa_dbar", "eps_embed"):
+            if prefix + name in g:
+                np.testing.assert_allclose([getattr(r, name) for r in recs], g[prefix + name], rtol=1e-8,
+                                           err_msg=prefix + name)
+            else:
+                assert all(getattr(r, name) is None for r in recs), prefix + name
+    gk = golden("krylov")
+    res = hs.gmres(hs.LinearOperator.from_matrix(gk["sq_M"]), gk["sq_b"], hs.SolverConfig(maxiter=15, compute_diagnostics=True))
+    np.testing.assert_allclose([r.kappa_basis for r in res.trace.records], gk["gm_kappa_basis"], rtol=1e-8)
+    res = hs.lsqr(hs.LinearOperator.from_matrix(gk["re_M"]), gk["re_b"], hs.SolverConfig(maxiter=15, compute_diagnostics=True))
+    np.testing.assert_allclose([r.kappa_basis for r in res.trace.records], gk["ls_kappa_basis"], rtol=1e-8)
+
+
 def _iterates(hs, K, b, S2, K_iter):
     out = []
     for k in range(1, K_iter + 1):
@@ -445,7 +478,7 @@ def test_validation_errors(hs):
     with pytest.raises(NotImplementedError):
         hs.slslu_tikhonov(A, np.ones(8), hs.SolverConfig(maxiter=2, lam=0.1), printed_f_columns=True)
     r = hs.scmrh(A, np.ones(8), hs.SolverConfig(maxiter=2, compute_diagnostics=True))
-    assert all(rec.res_norm is not None and rec.kappa_basis is None for rec in r.trace.records)
+    assert all(rec.res_norm is not None and rec.kappa_basis is not None for rec in r.trace.records)
 
 
 def test_deterministic_replay(hs):
