@@ -14,6 +14,7 @@
  *   hs_op_apply             LinearOperator.apply / apply_transpose   linops.py:107-125
  *   hs_sketch_create        SketchOperator / make_gaussian_sketch    sketch.py:29-53
  *   hs_sketch_apply         sketch_apply                             sketch.py:56-65
+ *   hs_sketch_apply_many    entries @ Q (a block of vectors)         sketch.py:108
  *   hs_solve                _hessenberg_solve                        solvers.py:410-539
  *                           via scmrh / slslu / *_tikhonov           solvers.py:562-605
  *                           and cmrh / lslu (unsketched)             solvers.py:542-559
@@ -140,6 +141,10 @@ int hs_sketch_create(hs_ctx* ctx, int kind, int64_t ell, int64_t in_rows, uint64
 int hs_sketch_create_csr(hs_ctx* ctx, int64_t ell, int64_t in_rows, int64_t nnz, const int64_t* indptr,
                          const int32_t* indices, const double* data, hs_sketch** out);
 int hs_sketch_apply(hs_sketch* sk, int work_dtype, const void* v, double* out);
+/* out[w*ell + i] = (S v_w)_i for nv vectors stored one after another (v[w*in_rows + c]);
+ * a Gaussian sketch generates S once per batch of up to 8 vectors.  Each column
+ * is bit-identical to hs_sketch_apply of that vector. */
+int hs_sketch_apply_many(hs_sketch* sk, int work_dtype, int32_t nv, const void* v, double* out);
 /* dense export (row-major ell x in_rows float64) */
 int hs_sketch_materialize(hs_sketch* sk, double* out);
 /* sparse-sign export as CSR (ell rows): indptr[ell+1], indices[nnz], data[nnz] */

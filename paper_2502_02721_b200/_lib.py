@@ -75,6 +75,7 @@ _SIGNATURES = [
     ("hs_sketch_create", c_i32, [c_vp, ctypes.c_int, c_i64, c_i64, ctypes.c_uint64, c_i32, c_vp, ctypes.POINTER(c_vp)]),
     ("hs_sketch_create_csr", c_i32, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, ctypes.POINTER(c_vp)]),
     ("hs_sketch_apply", c_i32, [c_vp, ctypes.c_int, c_vp, c_vp]),
+    ("hs_sketch_apply_many", c_i32, [c_vp, ctypes.c_int, c_i32, c_vp, c_vp]),
     ("hs_sketch_materialize", c_i32, [c_vp, c_vp]),
     ("hs_sketch_nnz", c_i32, [c_vp, P_i64]),
     ("hs_sketch_export_csr", c_i32, [c_vp, c_vp, c_vp, c_vp]),

@@ -19,6 +19,7 @@
 #include <map>
 #include <memory>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/hessketch_b200.h"
@@ -517,6 +518,21 @@ struct hs_op {
       dense_seq_gemv_kernel<V, Tin, T><<<grid_for(rows, 256, 1 << 30), 256, 1024 * sizeof(T), s>>>(rows, cols, Mcm,
                                                                                                    xi, yo);
       CKL();
+    } else if ((kw == 15 || kw == 31) && !env_flag("HS_PSF_SIMPLE")) {
+      Prof p(ctx, "psf_stencil", (double)H * W * (sizeof(Tin) + sizeof(T)));
+      auto launch = [&](auto kwc) {
+        constexpr int KWc = decltype(kwc)::value;
+        using G = PsfRb<T, KWc>;
+        const dim3 grid((W + G::TILE_X - 1) / G::TILE_X, (H + G::TY - 1) / G::TY);
+        const size_t smem = G::smem(kh);
+        auto kern = transpose ? psf_stencil_rb_kernel<V, Tin, T, KWc, G::R, G::TXT, G::TY, true>
+                              : psf_stencil_rb_kernel<V, Tin, T, KWc, G::R, G::TXT, G::TY, false>;
+        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<grid, G::TXT * G::TY, smem, s>>>(H, W, kh, K.as<V>(), xi, yo);
+        CKL();
+      };
+      if (kw == 15) launch(std::integral_constant<int, 15>());
+      else launch(std::integral_constant<int, 31>());
     } else {
       constexpr int TX = 32, TY = 8;
       dim3 grid((W + TX - 1) / TX, (H + TY - 1) / TY);
@@ -660,14 +676,7 @@ struct hs_sketch {
       sketch_dense_kernel<double, Tin><<<(int)ell, 256, 0, s>>>((int)ell, m, S.as<double>(), m, vi, z);
       CKL();
     } else if (kind == HS_SKETCH_GAUSSIAN) {
-      Prof p(ctx, "sketch_gauss", (double)m * sizeof(Tin), s);
-      const int nq = (int)((ell + 3) / 4);
-      dim3 grid(ntiles, (nq + 63) / 64);
-      sketch_gauss_partial_kernel<Tin><<<grid, 256, 0, s>>>((int)ell, m, 0, tile_cols, key(), vi, part.as<double>());
-      CKL();
-      sketch_tile_reduce_kernel<<<grid_for(ell, 128, 1 << 30), 128, 0, s>>>((int)ell, ntiles, part.as<double>(),
-                                                                            1.0 / std::sqrt((double)ell), z);
-      CKL();
+      apply_many_t<Tin>(v, 0, 1, z, 0, st);
     } else if (kind == 3) {
       Prof p(ctx, "sketch_csr", 0.0, s);
       sketch_csr_kernel<Tin><<<(int)ell, 256, 0, s>>>((int)ell, rowptr.as<long long>(), scol.as<int>(),
@@ -679,6 +688,29 @@ struct hs_sketch {
                                                          1.0 / std::sqrt((double)zeta), z);
       CKL();
     }
+  }
+  // z[:, w] = S v_w for nv vectors with column stride ldv (z column stride ldz).
+  // The Gaussian kind generates S once for the whole batch (hs_sketch.cuh);
+  // the other kinds apply column by column.  Results equal nv single applies.
+  template <class Tin>
+  void apply_many_t(const void* v, long long ldv, int nv, double* z, long long ldz, cudaStream_t st) const {
+    cudaStream_t s = st ? st : ctx->stream;
+    const Tin* vi = reinterpret_cast<const Tin*>(v);
+    if (kind == HS_SKETCH_GAUSSIAN) {
+      Prof p(ctx, "sketch_gauss", (double)nv * m * sizeof(Tin), s);
+      CK(cudaGetLastError());
+      g_launches += gauss_sketch_launch<Tin>(s, (int)ell, m, 0, tile_cols, key(), vi, ldv, nv, part.as<double>(), z,
+                                             ldz);
+      CK(cudaGetLastError());
+    } else {
+      for (int w = 0; w < nv; ++w) apply_t<Tin>(vi + (long long)w * ldv, z + (long long)w * ldz, st);
+    }
+  }
+  void apply_many(const void* v, int vdt, long long ldv, int nv, double* z, long long ldz,
+                  cudaStream_t st = nullptr) const {
+    if (vdt == HS_F64) apply_many_t<double>(v, ldv, nv, z, ldz, st);
+    else if (vdt == HS_F32) apply_many_t<float>(v, ldv, nv, z, ldz, st);
+    else apply_many_t<__nv_bfloat16>(v, ldv, nv, z, ldz, st);
   }
   void apply(const void* v, int vdt, double* z, cudaStream_t st = nullptr) const {
     if (vdt == HS_F64) apply_t<double>(v, z, st);
@@ -1113,6 +1145,54 @@ struct Solver {
       CK(cudaEventRecord(ev_l, s));
       CK(cudaStreamWaitEvent(s2, ev_l, 0));
     }
+    // Batched Gaussian sketches.  Nothing in the basis recurrence reads a
+    // sketch (pivots, H, W and the bases depend on A and b only), so the
+    // columns z_k = S2 A l_k (and f_k = S1 l_{k+1}) can be formed SB at a
+    // time: the operator writes u_k into a ring of 2*SB slots, and every SB
+    // iterations the aux stream sketches the SB slots with ONE pass of the
+    // counter-based generator (hs_sketch.cuh) and runs the SB projected solves.
+    // Each z_k is bit-identical to the per-iteration sketch; only the fused
+    // iterate lags (x_j rides on the basis pass of iteration j + 2*SB - 1,
+    // the last ones are formed after the loop).
+    const bool gauss_any = ovl && ((S2 && S2->kind == HS_SKETCH_GAUSSIAN) ||
+                                   (lamon && S1 && S1->kind == HS_SKETCH_GAUSSIAN));
+    int SB = 1;
+    if (gauss_any) {
+      const char* e = getenv("HS_SKETCH_BATCH");
+      SB = e && *e ? atoi(e) : GAUSS_NV_MAX;
+      SB = std::max(1, std::min(SB, std::max(1, K)));
+    }
+    const int xlag = SB > 1 ? 2 * SB - 1 : 1;
+    DBuf uring(SB > 1 ? (size_t)2 * SB * ldm * sizeof(T) : 0);
+    const int nbatch = (K + SB - 1) / SB;
+    std::vector<cudaEvent_t> ev_skb(SB > 1 ? nbatch : 0), ev_qrb(SB > 1 ? nbatch : 0);
+    for (auto& e : ev_skb) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : ev_qrb) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    std::vector<int> fused_at(K + 2, 0);  // iteration whose basis pass formed x_j
+    int flushed = 0;                       // iterations whose sketches / projected solves are queued
+    // sketch + projected solves of iterations flushed+1 .. kend_b on the aux stream
+    auto flush_batch = [&](int kend_b) {
+      if (kend_b <= flushed) return;
+      const int kb0 = flushed + 1, nb = kend_b - flushed;
+      const int bidx = (kb0 - 1) / SB;
+      CK(cudaEventRecord(ev_l, s));
+      CK(cudaStreamWaitEvent(s2, ev_l, 0));
+      const long long slot0 = (long long)((kb0 - 1) % (2 * SB));
+      S2->apply_many(uring.as<T>() + slot0 * ldm, wdt, ldm, nb, Zb.as<double>() + (long long)(kb0 - 1) * ell, ell, s2);
+      CK(cudaEventRecord(ev_skb[bidx], s2));
+      if (lamon) S1->apply_many(Lcol(kb0), bdt, ldn, nb, Fb.as<double>() + (long long)kb0 * ell, ell, s2);
+      for (int kk = kb0; kk <= kend_b; ++kk) {
+        qa.zcol = Zb.as<double>() + (long long)(kk - 1) * ell;
+        qa.fcol = lamon ? Fb.as<double>() + (long long)(kk - 1) * ell : nullptr;
+        Prof p(ctx, "qr_step", 0.0, s2);
+        int k1 = kk, it = kk;
+        void* args[] = {&qa, &k1, &it};
+        CK(cudaLaunchCooperativeKernel((void*)qr_step_kernel, dim3(NB), dim3(256), args, qr_smem, s2));
+        ++g_launches;
+      }
+      CK(cudaEventRecord(ev_qrb[bidx], s2));
+      flushed = kend_b;
+    };
 
     // host-side breakdown polling (pinned flag copied at the end of each iteration)
     int* hflag = nullptr;
@@ -1131,14 +1211,24 @@ struct Solver {
         if (hflag[k - 2] != 0) break;
       }
       k_last = k;
-      const int kx = (rec_x && k >= 2) ? k - 1 : 0;
-      const double* yprev = kx ? Yh.as<double>() + (long long)(k - 2) * K : nullptr;
-      double* relslot = kx ? rel2.as<double>() + (k - 2) : nullptr;
-      // u is free once the previous iteration's sketch has read it
-      if (ovl && k > 1) CK(cudaStreamWaitEvent(s, ev_sk, 0));
-      op->apply(Lcol(k - 1), bdt, u.p, wdt, false);
+      const int kx = (rec_x && k - xlag >= 1) ? k - xlag : 0;
+      const double* yprev = kx ? Yh.as<double>() + (long long)(kx - 1) * K : nullptr;
+      double* relslot = kx ? rel2.as<double>() + (kx - 1) : nullptr;
+      if (kx) fused_at[kx] = k;
+      T* const ucur = SB > 1 ? uring.as<T>() + (long long)((k - 1) % (2 * SB)) * ldm : u.as<T>();
+      if (SB > 1) {
+        // this half of the ring was last read by the sketch of batch bidx - 2
+        const int bidx = (k - 1) / SB;
+        if ((k - 1) % SB == 0 && bidx >= 2) CK(cudaStreamWaitEvent(s, ev_skb[bidx - 2], 0));
+      } else if (ovl && k > 1) {
+        // u is free once the previous iteration's sketch has read it
+        CK(cudaStreamWaitEvent(s, ev_sk, 0));
+      }
+      op->apply(Lcol(k - 1), bdt, ucur, wdt, false);
       if (diag_eps) qW.append(u.as<T>());  // the unreduced A l_k (solvers.py:480-481)
-      if (ovl) {
+      if (SB > 1) {
+        // sketched in batches (flush_batch)
+      } else if (ovl) {
         CK(cudaEventRecord(ev_u, s));
         CK(cudaStreamWaitEvent(s2, ev_u, 0));
         S2->apply(u.p, wdt, Zb.as<double>() + (long long)(k - 1) * ell, s2);
@@ -1148,11 +1238,11 @@ struct Solver {
       }
       // the fused iterate x_{k-1} needs y^{(k-1)} from the aux stream
       auto wait_y = [&] {
-        if (ovl && kx) CK(cudaStreamWaitEvent(s, ev_qr, 0));
+        if (ovl && kx) CK(cudaStreamWaitEvent(s, SB > 1 ? ev_qrb[(kx - 1) / SB] : ev_qr, 0));
       };
       if (!square) {
-        fsub(u.as<T>(), tpos.as<long long>(), PD.as<T>(), ldp, k, k, 0, cvec.as<T>(), Hcol(k - 1));
-        elim(u.as<T>(), m, ldm, D, k, 0, k, 0, nullptr, nullptr, uel);
+        fsub(ucur, tpos.as<long long>(), PD.as<T>(), ldp, k, k, 0, cvec.as<T>(), Hcol(k - 1));
+        elim(ucur, m, ldm, D, k, 0, k, 0, nullptr, nullptr, uel);
         sample(uel, m, k, 2 * k, 0, k);
         pivot_commit_kernel<T, B><<<1, 256, 0, s>>>(k, m, Hcol(k - 1), tpos.as<long long>(), PD.as<T>(), ldp, D, ldm,
                                                     0, m, st, 0, k, pv.as<T>());
@@ -1177,9 +1267,9 @@ struct Solver {
         CKL();
       } else {
         if (skd && !ovl && !sb) S2->apply(u.p, wdt, Zb.as<double>() + (long long)(k - 1) * ell);
-        fsub(u.as<T>(), tpos.as<long long>(), PL.as<T>(), ldp, k, k, 0, cvec.as<T>(), Hcol(k - 1));
+        fsub(ucur, tpos.as<long long>(), PL.as<T>(), ldp, k, k, 0, cvec.as<T>(), Hcol(k - 1));
         wait_y();
-        elim(u.as<T>(), n, ldn, L, k, 0, k, kx, yprev, relslot, uel);
+        elim(ucur, n, ldn, L, k, 0, k, kx, yprev, relslot, uel);
         sample(uel, n, k, k, 0, k);
         pivot_commit_kernel<T, B><<<1, 256, 0, s>>>(k, n, Hcol(k - 1), tpos.as<long long>(), PL.as<T>(), ldp, L, ldn,
                                                     0, n, st, 0, k, pv.as<T>());
@@ -1200,14 +1290,14 @@ struct Solver {
       }
       qa.zcol = Zb.as<double>() + (long long)(k - 1) * ell;
       qa.fcol = lamon ? Fb.as<double>() + (long long)(k - 1) * ell : nullptr;
-      {
+      if (SB == 1) {
         Prof p(ctx, "qr_step", 0.0, s2);
         int kk = k, it = k;
         void* args[] = {&qa, &kk, &it};
         CK(cudaLaunchCooperativeKernel((void*)qr_step_kernel, dim3(NB), dim3(256), args, qr_smem, s2));
         ++g_launches;
       }
-      if (ovl) CK(cudaEventRecord(ev_qr, s2));
+      if (ovl && SB == 1) CK(cudaEventRecord(ev_qr, s2));
       if (diag) {  // compute_diagnostics: x_k and |b - A x_k| (raw forward, uncounted; solvers.py:523-525)
         if (ovl) CK(cudaStreamWaitEvent(s, ev_qr, 0));
         xpass_kernel<B><<<grid_for(n, 256, SMS * 8), 256, (size_t)k * sizeof(double), s>>>(
@@ -1253,7 +1343,9 @@ struct Solver {
           CKL();
         }
       }
-      if (lamon) {
+      if (SB > 1) {
+        if (k % SB == 0) flush_batch(k);
+      } else if (lamon) {
         // F column k = S1 l_{k+1} (used by the projected solve of iteration k+1)
         if (ovl) {
           CK(cudaEventRecord(ev_l, s));
@@ -1265,6 +1357,7 @@ struct Solver {
       CK(cudaMemcpyAsync(hflag + k, &st->bd_iter, sizeof(int), cudaMemcpyDeviceToHost, s));
       CK(cudaEventRecord(flag_ev[k], s));
     }
+    if (SB > 1) flush_batch(k_last);
     // join the aux stream (last sketch / projected solve) before timing and readback
     cudaEvent_t ev_end;
     CK(cudaEventCreate(&ev_end));
@@ -1295,7 +1388,13 @@ struct Solver {
     };
     xpass(kend, xd.as<double>(), xt_h ? rel2.as<double>() + (kend - 1) : nullptr);
     const bool data_bd = bd_at && !square && hst.bd_side == 0;
-    if (rec_x && kend >= 2 && data_bd) xpass(kend - 1, nullptr, rel2.as<double>() + (kend - 2));
+    // iterates whose fused pass did not run (lagged past the end, or on the
+    // solution-side pass of an iteration whose data side broke down)
+    if (rec_x)
+      for (int j = 1; j < kend; ++j) {
+        const int f = fused_at[j];
+        if (!(f && (f < kend || (f == kend && !data_bd)))) xpass(j, nullptr, rel2.as<double>() + (j - 1));
+      }
     CK(cudaStreamSynchronize(s));
     float lms = 0;
     CK(cudaEventElapsedTime(&lms, ev[0], kend == k_last ? ev_end : ev[kend]));
@@ -1309,6 +1408,8 @@ struct Solver {
     for (auto& e : ev) cudaEventDestroy(e);
     for (auto& e : flag_ev) cudaEventDestroy(e);
     for (auto e : {ev_u, ev_sk, ev_qr, ev_l, ev_end}) cudaEventDestroy(e);
+    for (auto e : ev_skb) cudaEventDestroy(e);
+    for (auto e : ev_qrb) cudaEventDestroy(e);
     cudaFreeHost(hflag);
 
     // ---- copy back

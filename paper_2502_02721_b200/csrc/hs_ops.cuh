@@ -154,6 +154,71 @@ psf_stencil_kernel(int H, int W, int kh, int kw, const V* __restrict__ K,
   y[(long long)r * W + c] = acc;
 }
 
+// Register-blocked variant for the common odd widths (KW = 15, 31): each
+// thread owns R consecutive outputs of a row; per PSF row a it loads the
+// R + KW - 1 input values its outputs touch into registers once and then
+// walks the KW taps, so every tap value (a smem broadcast) feeds R products.
+// Each output still accumulates a-major / b-minor with the product rounded
+// before the add (Rn mul, Rn add): bit-identical to psf_stencil_kernel.
+template <class V, class Tin, class T, int KW, int R, int TXT, int TY, bool TR>
+__global__ void __launch_bounds__(TXT * TY)
+psf_stencil_rb_kernel(int H, int W, int kh, const V* __restrict__ K, const Tin* __restrict__ x,
+                      T* __restrict__ y) {
+  constexpr int rx = KW / 2;
+  constexpr int TILE_X = TXT * R;
+  constexpr int SW = ((TILE_X + 2 * rx + 3) / 4) * 4;  // row pitch (16-byte aligned rows)
+  constexpr int NW = R + KW - 1;                       // window per PSF row
+  const int ry = kh / 2;
+  const int SH = TY + 2 * ry;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* tile = reinterpret_cast<T*>(smem_raw);
+  T* ks = tile + SW * SH;
+  const int tx = threadIdx.x % TXT, ty = threadIdx.x / TXT;
+  const int c0 = blockIdx.x * TILE_X, r0 = blockIdx.y * TY;
+  for (int i = threadIdx.x; i < kh * KW; i += blockDim.x) ks[i] = cvt<T>(K[i]);
+  for (int i = threadIdx.x; i < SW * SH; i += blockDim.x) {
+    const int sr = i / SW, sc = i - sr * SW;
+    const int gr = r0 + sr - ry, gc = c0 + sc - rx;
+    T v = T(0);
+    if (sc < TILE_X + 2 * rx && gr >= 0 && gr < H && gc >= 0 && gc < W) v = cvt<T>(x[(long long)gr * W + gc]);
+    tile[i] = v;
+  }
+  __syncthreads();
+  const int r = r0 + ty, cb = c0 + tx * R;
+  if (r >= H || cb >= W) return;
+  T acc[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) acc[j] = T(0);
+  for (int a = 0; a < kh; ++a) {
+    const T* trow = tile + (TR ? (ty + a) : (ty + 2 * ry - a)) * SW + tx * R;
+    T w[NW];
+#pragma unroll
+    for (int q = 0; q < NW; ++q) w[q] = trow[q];
+    const T* krow = ks + a * KW;
+#pragma unroll
+    for (int b = 0; b < KW; ++b) {
+      const T kab = krow[b];
+#pragma unroll
+      for (int j = 0; j < R; ++j) acc[j] = Rn<T>::add(acc[j], Rn<T>::mul(kab, w[TR ? j + b : j + KW - 1 - b]));
+    }
+  }
+  T* yr = y + (long long)r * W + cb;
+#pragma unroll
+  for (int j = 0; j < R; ++j)
+    if (cb + j < W) yr[j] = acc[j];
+}
+
+template <class T, int KW> struct PsfRb {
+  static constexpr int R = sizeof(T) == 4 ? 8 : 4;
+  static constexpr int TXT = sizeof(T) == 4 ? 16 : 32;
+  static constexpr int TY = sizeof(T) == 4 ? 16 : 8;
+  static constexpr int TILE_X = TXT * R;
+  static size_t smem(int kh) {
+    const int SW = ((TILE_X + 2 * (KW / 2) + 3) / 4) * 4;
+    return ((size_t)SW * (TY + 2 * (kh / 2)) + (size_t)kh * KW) * sizeof(T);
+  }
+};
+
 }  // namespace hs
 
 namespace hs {

@@ -33,14 +33,21 @@ __device__ __forceinline__ void gauss_quad(uint2 key, unsigned long long c, unsi
 }
 
 // grid: (ntiles, nqb), block 256 = QB row quads x PH column phases (QB = quads
-// per block, chosen so the quads split evenly over the nqb blocks); the tile's
-// slice of v is staged in shared memory as fp64 (converted once per block)
-template <class Tin>
+// per block, chosen so the quads split evenly over the nqb blocks).  The tile's
+// slice of the nv <= NV input vectors (column stride ldv) is staged in shared
+// memory as fp64, vs[i*NV + w] (converted once per block), so every generated
+// quad of normals is applied to all nv vectors: a batch of nv sketches costs
+// one RNG pass instead of nv.  Per vector the columns each thread visits, the
+// fma order and the phase reduction do not depend on NV or nv, so a vector's
+// result is bit-identical whether it is sketched alone or in a batch.
+// part layout: part[(w * ntiles + tile) * ell + i].
+constexpr int GAUSS_CH = 1024;
+template <class Tin, int NV>
 __global__ void __launch_bounds__(256)
 sketch_gauss_partial_kernel(int ell, long long m, long long col_offset, long long tile_cols, uint2 key,
-                            const Tin* __restrict__ v, double* __restrict__ part) {
-  constexpr int CH = 1024;
-  __shared__ double vs[CH];
+                            const Tin* __restrict__ v, long long ldv, int nv, double* __restrict__ part) {
+  extern __shared__ __align__(128) unsigned char gauss_smem[];
+  double* vs = reinterpret_cast<double*>(gauss_smem);  // GAUSS_CH * NV
   __shared__ double red[256][4];
   const int nq = (ell + 3) / 4;
   const int nqb = gridDim.y;
@@ -51,37 +58,111 @@ sketch_gauss_partial_kernel(int ell, long long m, long long col_offset, long lon
   const bool active = ph < PH && q < nq;
   const long long c0 = (long long)blockIdx.x * tile_cols;
   const long long c1 = min(m, c0 + tile_cols);
-  double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-  for (long long cb = c0; cb < c1; cb += CH) {
-    const int cn = (int)min((long long)CH, c1 - cb);
+  double a[NV][4];
+#pragma unroll
+  for (int w = 0; w < NV; ++w) a[w][0] = a[w][1] = a[w][2] = a[w][3] = 0.0;
+  for (long long cb = c0; cb < c1; cb += GAUSS_CH) {
+    const int cn = (int)min((long long)GAUSS_CH, c1 - cb);
     __syncthreads();
-    for (int i = threadIdx.x; i < cn; i += blockDim.x) vs[i] = cvt<double>(v[cb + i]);
+    // vectors past nv are staged as zeros so the hot loop has no guards
+#pragma unroll
+    for (int w = 0; w < NV; ++w) {
+      const Tin* vw = v + (long long)w * ldv + cb;
+      for (int i = threadIdx.x; i < cn; i += blockDim.x) vs[i * NV + w] = w < nv ? cvt<double>(vw[i]) : 0.0;
+    }
     __syncthreads();
     if (active) {
+#pragma unroll 2
       for (int i = ph; i < cn; i += PH) {
-        const double vc = vs[i];
         float g[4];
         gauss_quad(key, (unsigned long long)(cb + i + col_offset), (unsigned)q, g);
-        a0 = fma((double)g[0], vc, a0);
-        a1 = fma((double)g[1], vc, a1);
-        a2 = fma((double)g[2], vc, a2);
-        a3 = fma((double)g[3], vc, a3);
-      }
-    }
-  }
-  red[threadIdx.x][0] = a0; red[threadIdx.x][1] = a1; red[threadIdx.x][2] = a2; red[threadIdx.x][3] = a3;
-  __syncthreads();
-  if (ph == 0 && q < nq) {
+        const double g0 = (double)g[0], g1 = (double)g[1], g2 = (double)g[2], g3 = (double)g[3];
+        if constexpr (NV == 1) {
+          const double vc = vs[i];
+          a[0][0] = fma(g0, vc, a[0][0]);
+          a[0][1] = fma(g1, vc, a[0][1]);
+          a[0][2] = fma(g2, vc, a[0][2]);
+          a[0][3] = fma(g3, vc, a[0][3]);
+        } else {
+          const double2* vp = reinterpret_cast<const double2*>(vs + i * NV);
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int i = 4 * q + r;
-      if (i < ell) {
-        double s = 0.0;
-        for (int p = 0; p < PH; ++p) s += red[p * QB + ql][r];  // fixed phase order
-        part[(long long)blockIdx.x * ell + i] = s;
+          for (int w2 = 0; w2 < NV / 2; ++w2) {
+            const double2 vv = vp[w2];
+            a[2 * w2][0] = fma(g0, vv.x, a[2 * w2][0]);
+            a[2 * w2][1] = fma(g1, vv.x, a[2 * w2][1]);
+            a[2 * w2][2] = fma(g2, vv.x, a[2 * w2][2]);
+            a[2 * w2][3] = fma(g3, vv.x, a[2 * w2][3]);
+            a[2 * w2 + 1][0] = fma(g0, vv.y, a[2 * w2 + 1][0]);
+            a[2 * w2 + 1][1] = fma(g1, vv.y, a[2 * w2 + 1][1]);
+            a[2 * w2 + 1][2] = fma(g2, vv.y, a[2 * w2 + 1][2]);
+            a[2 * w2 + 1][3] = fma(g3, vv.y, a[2 * w2 + 1][3]);
+          }
+        }
       }
     }
   }
+#pragma unroll
+  for (int w = 0; w < NV; ++w) {
+    if (w >= nv) break;
+    __syncthreads();
+    red[threadIdx.x][0] = a[w][0]; red[threadIdx.x][1] = a[w][1];
+    red[threadIdx.x][2] = a[w][2]; red[threadIdx.x][3] = a[w][3];
+    __syncthreads();
+    if (ph == 0 && q < nq) {
+      double* pw = part + ((long long)w * gridDim.x + blockIdx.x) * ell;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int i = 4 * q + r;
+        if (i < ell) {
+          double s = 0.0;
+          for (int p = 0; p < PH; ++p) s += red[p * QB + ql][r];  // fixed phase order
+          pw[i] = s;
+        }
+      }
+    }
+  }
+}
+
+// largest batch one partial launch handles
+constexpr int GAUSS_NV_MAX = 8;
+
+// launch the partial + reduce pair for nv vectors (column stride ldv) into
+// z[w * ldz + i]; batches larger than GAUSS_NV_MAX go in groups
+template <class Tin, int NV>
+inline void gauss_partial_launch(dim3 grid, cudaStream_t s, int ell, long long m, long long col_offset,
+                                 long long tile_cols, uint2 key, const Tin* v, long long ldv, int nv, double* part) {
+  const size_t smem = (size_t)GAUSS_CH * NV * sizeof(double);
+  static bool attr = false;  // per instantiation
+  if (!attr && smem > 48 * 1024) {
+    cudaFuncSetAttribute(sketch_gauss_partial_kernel<Tin, NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  sketch_gauss_partial_kernel<Tin, NV><<<grid, 256, smem, s>>>(ell, m, col_offset, tile_cols, key, v, ldv, nv, part);
+}
+
+__global__ void sketch_tile_reduce_kernel(int ell, int ntiles, const double* __restrict__ part, double scale,
+                                          double* __restrict__ z, long long ldz);
+
+template <class Tin>
+inline int gauss_sketch_launch(cudaStream_t s, int ell, long long m, long long col_offset, long long tile_cols,
+                               uint2 key, const Tin* v, long long ldv, int nv, double* part, double* z,
+                               long long ldz) {
+  const int nq = (ell + 3) / 4;
+  const int ntl = (int)((m + tile_cols - 1) / tile_cols);
+  const dim3 grid(ntl, (nq + 63) / 64);
+  int launches = 0;
+  for (int w0 = 0; w0 < nv; w0 += GAUSS_NV_MAX) {
+    const int g = nv - w0 < GAUSS_NV_MAX ? nv - w0 : GAUSS_NV_MAX;
+    const Tin* vg = v + (long long)w0 * ldv;
+    if (g == 1) gauss_partial_launch<Tin, 1>(grid, s, ell, m, col_offset, tile_cols, key, vg, ldv, g, part);
+    else if (g == 2) gauss_partial_launch<Tin, 2>(grid, s, ell, m, col_offset, tile_cols, key, vg, ldv, g, part);
+    else if (g <= 4) gauss_partial_launch<Tin, 4>(grid, s, ell, m, col_offset, tile_cols, key, vg, ldv, g, part);
+    else gauss_partial_launch<Tin, 8>(grid, s, ell, m, col_offset, tile_cols, key, vg, ldv, g, part);
+    sketch_tile_reduce_kernel<<<dim3((ell + 127) / 128, g), 128, 0, s>>>(ell, ntl, part, 1.0 / sqrt((double)ell),
+                                                                         z + (long long)w0 * ldz, ldz);
+    launches += 2;
+  }
+  return launches;
 }
 
 // number of row-quad blocks for the partial kernel (<= 64 quads per block, balanced)
@@ -90,14 +171,15 @@ inline int gauss_quad_blocks(int ell) {
   return (nq + 63) / 64;
 }
 
-// z[i] = scale * sum_t part[t][i]   (t ascending)
+// z[w * ldz + i] = scale * sum_t part[w][t][i]   (t ascending); grid.y = vector
 __global__ void sketch_tile_reduce_kernel(int ell, int ntiles, const double* __restrict__ part, double scale,
-                                          double* __restrict__ z) {
+                                          double* __restrict__ z, long long ldz) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= ell) return;
+  const double* pw = part + (long long)blockIdx.y * ntiles * ell;
   double s = 0.0;
-  for (int t = 0; t < ntiles; ++t) s += part[(long long)t * ell + i];
-  z[i] = s * scale;
+  for (int t = 0; t < ntiles; ++t) s += pw[(long long)t * ell + i];
+  z[(long long)blockIdx.y * ldz + i] = s * scale;
 }
 
 // materialise the generated Gaussian S (row-major ell x m, fp64) for export

@@ -86,11 +86,23 @@ class DeviceSketch:
         return (self.out_rows, self.in_rows)
 
     def apply(self, v, dtype=np.float64):
+        v = np.asarray(v)
+        code = _lib.HS_F64 if np.dtype(dtype) == np.float64 else _lib.HS_F32
+        if v.ndim == 2:
+            # entries @ Q for a block of columns (sketch.py:108): one generator
+            # pass per 8 columns for the Gaussian kind, each column bit-identical
+            # to a single apply
+            if v.shape[0] != self.in_rows:
+                raise ValueError(f"sketch expects {self.in_rows} rows, got shape {v.shape}")
+            vt = np.ascontiguousarray(v.T, dtype=dtype)
+            out = np.empty((v.shape[1], self.out_rows))
+            _lib.check(_lib.load().hs_sketch_apply_many(self._handle, code, int(v.shape[1]), _lib.ptr(vt),
+                                                        _lib.ptr(out)))
+            return np.ascontiguousarray(out.T)
         v = np.ascontiguousarray(v, dtype=dtype)
         if v.shape != (self.in_rows,):
             raise ValueError(f"sketch expects a vector of length {self.in_rows}, got shape {v.shape}")
         out = np.empty(self.out_rows)
-        code = _lib.HS_F64 if np.dtype(dtype) == np.float64 else _lib.HS_F32
         _lib.check(_lib.load().hs_sketch_apply(self._handle, code, _lib.ptr(v), _lib.ptr(out)))
         return out
 

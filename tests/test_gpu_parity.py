@@ -91,7 +91,8 @@ def test_dense_operator_bitwise_sequential(hs):
 
 
 @pytest.mark.parametrize("dt", [np.float64, np.float32])
-@pytest.mark.parametrize("shape,ks", [((16, 16), (5, 5)), ((33, 70), (3, 7)), ((64, 64), (15, 15))])
+@pytest.mark.parametrize("shape,ks", [((16, 16), (5, 5)), ((33, 70), (3, 7)), ((64, 64), (15, 15)),
+                                      ((150, 270), (31, 31)), ((37, 129), (9, 15)), ((70, 300), (31, 15))])
 def test_psf_stencil_bitwise(hs, dt, shape, ks):
     rng = np.random.default_rng(5)
     K = rng.random(ks)
@@ -646,5 +647,8 @@ def test_sharded_path_single_rank(hs, lam, basis):
     np.testing.assert_array_equal(f2.L_matrix(), f1.L_matrix())
     np.testing.assert_array_equal(r2.x, r1.x)
     assert r2.trace.column("sres_norm") == r1.trace.column("sres_norm")
-    assert r2.trace.column("rel_err") == r1.trace.column("rel_err")
+    # rel_err: the single-GPU path sketches the Gaussian S1 in batches, so its
+    # last iterates' errors come from the fp64 x pass instead of the fused
+    # (fp32-accumulated) one -- equal to rounding, not bitwise
+    np.testing.assert_allclose(r2.trace.column("rel_err"), r1.trace.column("rel_err"), rtol=1e-6)
     assert r2.trace.column("sketches") == r1.trace.column("sketches")
