@@ -18,6 +18,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <type_traits>
 #include <vector>
@@ -193,6 +194,43 @@ struct hs_ctx {
     cudaEvent_t e;
     CK(cudaEventCreate(&e));
     return e;
+  }
+  // per-solve events and pinned scratch, kept across solves: creating and
+  // destroying ~600 events and a pinned buffer per solve sporadically cost
+  // ~0.25 s of host time (measured, tools/e2e_breakdown.py)
+  std::vector<cudaEvent_t> pool_timed, pool_sync;
+  std::mutex solve_mu;  // solves on one context are serialised (they share its streams and scratch)
+  void* pinned = nullptr;
+  size_t pinned_cap = 0;
+  std::vector<cudaEvent_t> take_events(size_t n, bool timed) {
+    auto& pool = timed ? pool_timed : pool_sync;
+    std::vector<cudaEvent_t> out;
+    out.reserve(n);
+    while (out.size() < n && !pool.empty()) {
+      out.push_back(pool.back());
+      pool.pop_back();
+    }
+    while (out.size() < n) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, timed ? cudaEventDefault : cudaEventDisableTiming));
+      out.push_back(e);
+    }
+    return out;
+  }
+  void give_events(std::vector<cudaEvent_t>& v, bool timed) {
+    auto& pool = timed ? pool_timed : pool_sync;
+    pool.insert(pool.end(), v.begin(), v.end());
+    v.clear();
+  }
+  void* pinned_buf(size_t bytes) {
+    if (bytes > pinned_cap) {
+      if (pinned) CK(cudaFreeHost(pinned));
+      pinned = nullptr;
+      pinned_cap = 0;
+      CK(cudaMallocHost(&pinned, bytes));
+      pinned_cap = bytes;
+    }
+    return pinned;
   }
   void harvest() {
     if (pending.empty()) return;
@@ -1096,8 +1134,17 @@ struct Solver {
     if (timing) CK(cudaStreamSynchronize(s));
     const auto t_init = now();
     // ---- the loop (solvers.py:468-538)
-    std::vector<cudaEvent_t> ev(K + 1);
-    for (auto& e : ev) CK(cudaEventCreate(&e));
+    std::vector<cudaEvent_t> ev = ctx->take_events(K + 2, true);  // ev[K + 1]: end of loop
+    std::vector<cudaEvent_t> sev = ctx->take_events(4, false);
+    std::vector<cudaEvent_t> flag_ev, ev_skb, ev_qrb;
+    struct Lease {  // events go back to the context pool on every exit path
+      hs_ctx* c;
+      std::vector<std::vector<cudaEvent_t>*> timed, sync;
+      ~Lease() {
+        for (auto* v : timed) c->give_events(*v, true);
+        for (auto* v : sync) c->give_events(*v, false);
+      }
+    } lease{ctx, {&ev}, {&sev, &flag_ev, &ev_skb, &ev_qrb}};
     QrArgs qa;
     qa.ell = (int)ell; qa.Ls = Ls; qa.ldq = ldq; qa.kmax = K; qa.lam = cfg.lam;
     qa.Z = Zb.as<double>(); qa.F = lamon ? Fb.as<double>() : nullptr; qa.sr0 = sr0.as<double>();
@@ -1136,11 +1183,7 @@ struct Solver {
     cudaStream_t s2 = ovl ? ctx->aux : s;
     DBuf u2(ovl ? ldm * sizeof(T) : 0);
     T* uel = ovl ? u2.as<T>() : u.as<T>();  // elimination output on the side that is sketched
-    cudaEvent_t ev_u, ev_sk, ev_qr, ev_l;
-    CK(cudaEventCreateWithFlags(&ev_u, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&ev_sk, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&ev_qr, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&ev_l, cudaEventDisableTiming));
+    cudaEvent_t ev_u = sev[0], ev_sk = sev[1], ev_qr = sev[2], ev_l = sev[3];
     if (ovl) {  // the aux stream starts after the init work (sr0, F col 0) on the main stream
       CK(cudaEventRecord(ev_l, s));
       CK(cudaStreamWaitEvent(s2, ev_l, 0));
@@ -1165,9 +1208,8 @@ struct Solver {
     const int xlag = SB > 1 ? 2 * SB - 1 : 1;
     DBuf uring(SB > 1 ? (size_t)2 * SB * ldm * sizeof(T) : 0);
     const int nbatch = (K + SB - 1) / SB;
-    std::vector<cudaEvent_t> ev_skb(SB > 1 ? nbatch : 0), ev_qrb(SB > 1 ? nbatch : 0);
-    for (auto& e : ev_skb) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    for (auto& e : ev_qrb) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ev_skb = ctx->take_events(SB > 1 ? nbatch : 0, false);
+    ev_qrb = ctx->take_events(SB > 1 ? nbatch : 0, false);
     std::vector<int> fused_at(K + 2, 0);  // iteration whose basis pass formed x_j
     int flushed = 0;                       // iterations whose sketches / projected solves are queued
     // sketch + projected solves of iterations flushed+1 .. kend_b on the aux stream
@@ -1195,11 +1237,13 @@ struct Solver {
     };
 
     // host-side breakdown polling (pinned flag copied at the end of each iteration)
-    int* hflag = nullptr;
-    CK(cudaMallocHost(&hflag, sizeof(int) * (K + 1)));
+    // pinned scratch: breakdown flags, then the staging area for x
+    const size_t flag_bytes = round_up(sizeof(int) * (K + 1), 4096);
+    char* pin = reinterpret_cast<char*>(ctx->pinned_buf(flag_bytes + (size_t)n * sizeof(double)));
+    int* hflag = reinterpret_cast<int*>(pin);
+    double* xstage = reinterpret_cast<double*>(pin + flag_bytes);
     for (int i = 0; i <= K; ++i) hflag[i] = 0;
-    std::vector<cudaEvent_t> flag_ev(K + 1);
-    for (auto& e : flag_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    flag_ev = ctx->take_events(K + 1, false);
 
     CK(cudaEventRecord(ev[0], s));
     int k_last = 0;
@@ -1359,8 +1403,7 @@ struct Solver {
     }
     if (SB > 1) flush_batch(k_last);
     // join the aux stream (last sketch / projected solve) before timing and readback
-    cudaEvent_t ev_end;
-    CK(cudaEventCreate(&ev_end));
+    cudaEvent_t ev_end = ev[K + 1];
     if (ovl) {
       CK(cudaEventRecord(ev_sk, s2));
       CK(cudaStreamWaitEvent(s, ev_sk, 0));
@@ -1396,6 +1439,7 @@ struct Solver {
         if (!(f && (f < kend || (f == kend && !data_bd)))) xpass(j, nullptr, rel2.as<double>() + (j - 1));
       }
     CK(cudaStreamSynchronize(s));
+    const auto t_xpass = now();
     float lms = 0;
     CK(cudaEventElapsedTime(&lms, ev[0], kend == k_last ? ev_end : ev[kend]));
     res->loop_ms = lms;
@@ -1405,16 +1449,13 @@ struct Solver {
       CK(cudaEventElapsedTime(&w, ev[k - 1], (k == kend && kend == k_last) ? ev_end : ev[k]));
       res->wall_ms[k - 1] = w;
     }
-    for (auto& e : ev) cudaEventDestroy(e);
-    for (auto& e : flag_ev) cudaEventDestroy(e);
-    for (auto e : {ev_u, ev_sk, ev_qr, ev_l, ev_end}) cudaEventDestroy(e);
-    for (auto e : ev_skb) cudaEventDestroy(e);
-    for (auto e : ev_qrb) cudaEventDestroy(e);
-    cudaFreeHost(hflag);
+    const auto t_events = now();
 
     // ---- copy back
-    res->x.resize(n);
-    CK(cudaMemcpy(res->x.data(), xd.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpyAsync(xstage, xd.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    res->x.assign(xstage, xstage + n);
+    const auto t_xcopy = now();
     res->sres.resize(kend);
     res->proj.resize(kend);
     res->rankfb.resize(kend);
@@ -1508,8 +1549,10 @@ struct Solver {
     res->ldm = ldm;
     if (timing) {
       const auto t_end = now();
-      fprintf(stderr, "[hs_solve] alloc %.1f ms, init %.1f ms, loop %.1f ms (device %.1f), finalize %.1f ms\n",
-              ms(t_start, t_alloc), ms(t_alloc, t_init), ms(t_init, t_loop), res->loop_ms, ms(t_loop, t_end));
+      fprintf(stderr, "[hs_solve] alloc %.1f ms, init %.1f ms, loop %.1f ms (device %.1f), finalize %.1f ms "
+              "(xpass %.1f, events %.1f, x copy %.1f, rest %.1f)\n",
+              ms(t_start, t_alloc), ms(t_alloc, t_init), ms(t_init, t_loop), res->loop_ms, ms(t_loop, t_end),
+              ms(t_loop, t_xpass), ms(t_xpass, t_events), ms(t_events, t_xcopy), ms(t_xcopy, t_end));
     }
   }
 
@@ -1559,6 +1602,9 @@ int hs_ctx_destroy(hs_ctx* ctx) {
       cudaEventDestroy(p.b);
     }
     for (auto e : ctx->free_events) cudaEventDestroy(e);
+    for (auto e : ctx->pool_timed) cudaEventDestroy(e);
+    for (auto e : ctx->pool_sync) cudaEventDestroy(e);
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->device < 64 && g_dev_stream[ctx->device] == ctx->stream) g_dev_stream[ctx->device] = nullptr;
     cudaStreamSynchronize(ctx->aux);
     cudaStreamDestroy(ctx->aux);
