@@ -1151,7 +1151,9 @@ struct Solver {
     qa.Q = Qb.as<double>(); qa.Rinv = Rinv.as<double>(); qa.Rdiag = Rdiag.as<double>(); qa.y = yb.as<double>();
     qa.Yhist = Yh.as<double>(); qa.part = part.as<double>(); qa.sres = sresb.as<double>(); qa.proj = projb.as<double>();
     qa.rankfb = rfb.as<int>(); qa.st = st;
-    const size_t qr_smem = ((size_t)((Ls + NB - 1) / NB) + 2 * (size_t)K) * sizeof(double);
+    DBuf Nnull((size_t)K * K * sizeof(double)), ndrop(sizeof(int));
+    qa.Nnull = Nnull.as<double>(); qa.ndrop = ndrop.as<int>();
+    const size_t qr_smem = qr_smem_bytes(Ls, NB, K);
     if (qr_smem > 48 * 1024)
       CK(cudaFuncSetAttribute(qr_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qr_smem));
     const bool rec_x = cfg.record_x && xt_h;

@@ -13,11 +13,20 @@
 // the stacked system, 5 grid-wide barriers.  Then sres = |Z y - S r0| and
 // proj_obj = sqrt(sres^2 + lam^2 |F y|^2) exactly as solvers.py:514-520 form them.
 //
-// Rank test: the reference raises RankDeficiencyError when min|R_ii| <
-// 1e-14 max|R_ii| of the PIVOTED QR (linops.py:197-203) and falls back to lstsq
-// (solvers.py:211-218).  This kernel applies the same 1e-14 test to the
-// unpivoted rho's, flags rank_fallback, and drops the dependent column (its
-// coefficient is set to 0).  The gate never fired in any survey probe.
+// Rank test and fallback: the reference raises RankDeficiencyError when
+// min|R_ii| < 1e-14 max|R_ii| of the PIVOTED QR (linops.py:197-203) and then
+// takes the minimum-norm least-squares solution (np.linalg.lstsq, solvers.py:
+// 211-218); once the sketched system is deficient it stays deficient, so every
+// later iteration takes the fallback too.  Here the same 1e-14 test is applied
+// to the new column's rho.  A dependent column j is dropped from the QR (zero
+// Q column, zero R^{-1} row/column), which makes y_b, the solution the update
+// formula carries, the BASIC solution (y_j = 0).  Its null vector
+// n_j = e_j - R^{-1} r_j (r_j = the column's coefficients against Q) is
+// orthonormalised (CGS2) against the earlier ones into Nnull, and the reported
+// solution is the minimum-norm one, y = y_b - N (N^T y_b): the lstsq answer
+// with the dependent directions truncated.  rank_fallback is set from the
+// first dropped column on, as in the reference (tests/test_gpu_parity.py:
+// test_rank_fallback_min_norm_vs_reference).
 #pragma once
 
 #include <cooperative_groups.h>
@@ -44,8 +53,15 @@ struct QrArgs {
   double* sres;         // kmax
   double* proj;         // kmax
   int* rankfb;          // kmax
+  double* Nnull = nullptr;  // kmax x kmax: orthonormal null vectors of the dropped columns
+  int* ndrop = nullptr;     // number of dropped columns so far
   LoopState* st;
 };
+
+// dynamic shared memory of qr_step_kernel
+inline size_t qr_smem_bytes(int Ls, int NB, int kmax) {
+  return ((size_t)((Ls + NB - 1) / NB) + 4 * (size_t)kmax) * sizeof(double);
+}
 
 __global__ void __launch_bounds__(256) qr_step_kernel(QrArgs a, int k, int iter) {
   namespace cg = cooperative_groups;
@@ -66,6 +82,8 @@ __global__ void __launch_bounds__(256) qr_step_kernel(QrArgs a, int k, int iter)
   double* av = sm;            // RS
   double* cv = sm + RS;       // kmax (c1, then c2)
   double* c1s = cv + a.kmax;  // kmax (saved c1)
+  double* wv = c1s + a.kmax;  // kmax (R^{-1} r of the new column / null vector)
+  double* gv = wv + a.kmax;   // kmax (projection coefficients)
   __shared__ double scratch[32];
 
   // phase 1: load the new stacked column, partial Q^T a
@@ -152,20 +170,70 @@ __global__ void __launch_bounds__(256) qr_step_kernel(QrArgs a, int k, int iter)
       a.Rinv[(long long)j * a.kmax + i] = deficient ? 0.0 : -s / rho;
       a.y[i] = yi;
       a.Yhist[(long long)j * a.kmax + i] = yi;
+      wv[i] = -s;
     }
     if (tid == 0) {
       a.Rinv[(long long)j * a.kmax + j] = deficient ? 0.0 : 1.0 / rho;
       a.Rdiag[j] = deficient ? 0.0 : rho;
       a.y[j] = eta;
       a.Yhist[(long long)j * a.kmax + j] = eta;
-      a.rankfb[j] = deficient ? 1 : 0;
+      wv[j] = 1.0;
     }
+    __syncthreads();
+    int d = *a.ndrop;  // uniform
+    double* N = a.Nnull;
+    if (deficient) {
+      // n_j = e_j - R^{-1} r_j, orthonormalised against the earlier null vectors (CGS2)
+      for (int pass = 0; pass < 2 && d > 0; ++pass) {
+        for (int t = warp; t < d; t += nwarps) {
+          const double* nt = N + (long long)t * a.kmax;
+          double s = 0.0;
+          for (int i = lane; i <= j; i += 32) s = fma(nt[i], wv[i], s);
+          s = warp_sum(s);
+          if (lane == 0) gv[t] = s;
+        }
+        __syncthreads();
+        for (int i = tid; i <= j; i += BT) {
+          double s = 0.0;
+          for (int t = 0; t < d; ++t) s = fma(N[(long long)t * a.kmax + i], gv[t], s);
+          wv[i] -= s;
+        }
+        __syncthreads();
+      }
+      double nn2 = 0.0;
+      for (int i = tid; i <= j; i += BT) nn2 = fma(wv[i], wv[i], nn2);
+      nn2 = block_sum(nn2, scratch);
+      const double inv = 1.0 / sqrt(nn2);
+      double* nd = N + (long long)d * a.kmax;
+      for (int i = tid; i < a.kmax; i += BT) nd[i] = i <= j ? wv[i] * inv : 0.0;
+      ++d;
+      __syncthreads();
+      if (tid == 0) *a.ndrop = d;
+    }
+    if (d > 0) {
+      // minimum-norm solution: y = y_b - N (N^T y_b)
+      double* yh = a.Yhist + (long long)j * a.kmax;
+      for (int t = warp; t < d; t += nwarps) {
+        const double* nt = N + (long long)t * a.kmax;
+        double s = 0.0;
+        for (int i = lane; i <= j; i += 32) s = fma(nt[i], yh[i], s);
+        s = warp_sum(s);
+        if (lane == 0) gv[t] = s;
+      }
+      __syncthreads();
+      for (int i = tid; i <= j; i += BT) {
+        double s = 0.0;
+        for (int t = 0; t < d; ++t) s = fma(N[(long long)t * a.kmax + i], gv[t], s);
+        yh[i] -= s;
+      }
+    }
+    if (tid == 0) a.rankfb[j] = d > 0 ? 1 : 0;
   }
   grid.sync();
 
   // phase 5: residual partials |Z y - sr0|^2 (top) and |F y|^2 (bottom)
   double* ys = cv;
-  for (int i = tid; i <= j; i += BT) ys[i] = __ldcg(&a.y[i]);
+  for (int i = tid; i <= j; i += BT) ys[i] = __ldcg(&a.Yhist[(long long)j * a.kmax + i]);
   __syncthreads();
   double s_top = 0.0, s_bot = 0.0;
   for (int r = tid; r < nr; r += BT) {

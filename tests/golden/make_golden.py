@@ -439,8 +439,43 @@ def gen_diagnostics():
     _save("diagnostics", **o)
 
 
+def gen_rank_fallback():
+    """Low-rank operators: the sketched projected system becomes rank deficient
+    (pivoted-QR gate, linops.py:197-203) and the reference takes the lstsq
+    minimum-norm fallback from then on (solvers.py:204-218)."""
+    rng = np.random.default_rng(0)
+    o = {}
+    n = 20
+    M = rng.standard_normal((n, 3)) @ rng.standard_normal((3, n))
+    b = rng.standard_normal(n)
+    xt = rng.standard_normal(n)
+    # stored as CSR: past the operator's rank the remainders are rounding noise,
+    # so the pivots match only under the sequential csr_matvec order the
+    # device reproduces bit for bit
+    A = LinearOperator.from_matrix(scipy.sparse.csr_matrix(M))
+    o.update(sq_M=M, sq_b=b, sq_xt=xt)
+    o.update(_pack_result(solvers.scmrh(A, b, solvers.SolverConfig(maxiter=8, sketch_rows=40, seed=1), x_true=xt),
+                          "sq_"))
+    o.update(_pack_result(solvers.cmrh(A, b, solvers.SolverConfig(maxiter=8), x_true=xt), "cm_"))
+    m = 30
+    Mr = rng.standard_normal((m, 4)) @ rng.standard_normal((4, n))
+    br = rng.standard_normal(m)
+    Ar = LinearOperator.from_matrix(scipy.sparse.csr_matrix(Mr))
+    o.update(re_M=Mr, re_b=br)
+    o.update(_pack_result(solvers.slslu(Ar, br, solvers.SolverConfig(maxiter=9, sketch_rows=40, seed=3), x_true=xt),
+                          "re_"))
+    o.update(_pack_result(solvers.lslu(Ar, br, solvers.SolverConfig(maxiter=9), x_true=xt), "ll_"))
+    for p in ("sq_", "cm_", "re_", "ll_"):
+        print(p, "rank_fallback", o[p + "rank_fallback"].astype(int), o[p + "termination"])
+    _save("rank_fallback", **o)
+
+
 if __name__ == "__main__":
     print("reference hessketch", hessketch.__version__)
+    if len(sys.argv) > 1:  # regenerate selected fixtures only: make_golden.py gen_rank_fallback ...
+        for name in sys.argv[1:]:
+            globals()[name]()
+        sys.exit(0)
     gen_pivot_and_steps()
     gen_scmrh_dense()
     gen_slslu_dense()
@@ -451,3 +486,4 @@ if __name__ == "__main__":
     gen_exchange()
     gen_krylov()
     gen_diagnostics()
+    gen_rank_fallback()

@@ -468,6 +468,27 @@ def test_edge_cases_vs_reference(hs, golden):
     _check(res, g, "tie_", bitwise_basis=False)
 
 
+def test_rank_fallback_min_norm_vs_reference(hs, golden):
+    """Low-rank operators make the sketched (and the unsketched) projected
+    system rank deficient; the reference flags rank_fallback from the first
+    deficient iteration on and returns the lstsq minimum-norm solution
+    (solvers.py:204-218).  Device: dropped dependent columns + null-space
+    projection (hs_qr.cuh).  Flags exact; residuals and iterates within 1e-8."""
+    g = golden("rank_fallback")
+    A = hs.LinearOperator.from_matrix(scipy.sparse.csr_matrix(g["sq_M"]))
+    Ar = hs.LinearOperator.from_matrix(scipy.sparse.csr_matrix(g["re_M"]))
+    cases = [
+        ("sq_", hs.scmrh(A, g["sq_b"], hs.SolverConfig(maxiter=8, sketch_rows=40, seed=1), x_true=g["sq_xt"])),
+        ("cm_", hs.cmrh(A, g["sq_b"], hs.SolverConfig(maxiter=8), x_true=g["sq_xt"])),
+        ("re_", hs.slslu(Ar, g["re_b"], hs.SolverConfig(maxiter=9, sketch_rows=40, seed=3), x_true=g["sq_xt"])),
+        ("ll_", hs.lslu(Ar, g["re_b"], hs.SolverConfig(maxiter=9), x_true=g["sq_xt"])),
+    ]
+    for p, res in cases:
+        assert [r.rank_fallback for r in res.trace.records] == list(g[p + "rank_fallback"]), p
+        assert any(g[p + "rank_fallback"])
+        _check(res, g, p, bitwise_basis=False, rtol=1e-8)
+
+
 def test_validation_errors(hs):
     A = hs.LinearOperator.from_matrix(np.eye(8) * 2.0 + 0.1)
     with pytest.raises(ValueError):

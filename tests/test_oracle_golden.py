@@ -256,6 +256,22 @@ def test_sampled_pivoting_and_unsketched_bitwise(golden):
     _check_result(res, g, "tomo_lslu_")
 
 
+def test_rank_fallback_bitwise(golden):
+    """Low-rank operators: pivoted-QR rank gate and lstsq minimum-norm fallback
+    from the first deficient iteration on (solvers.py:204-218)."""
+    g = golden("rank_fallback")
+    A = ho.csr_operator(scipy.sparse.csr_matrix(g["sq_M"]))
+    res = ho.hessenberg_solve(A, g["sq_b"], square=True, maxiter=8, seed=1, ell=40, x_true=g["sq_xt"])
+    _check_result(res, g, "sq_")
+    res = ho.hessenberg_solve(A, g["sq_b"], square=True, maxiter=8, x_true=g["sq_xt"], sketched=False)
+    _check_result(res, g, "cm_")
+    Ar = ho.csr_operator(scipy.sparse.csr_matrix(g["re_M"]))
+    res = ho.hessenberg_solve(Ar, g["re_b"], square=False, maxiter=9, seed=3, ell=40, x_true=g["sq_xt"])
+    _check_result(res, g, "re_")
+    res = ho.hessenberg_solve(Ar, g["re_b"], square=False, maxiter=9, x_true=g["sq_xt"], sketched=False)
+    _check_result(res, g, "ll_")
+
+
 def _check_krylov(res, g, prefix):
     assert res.termination == str(g[prefix + "termination"])
     assert len(res.records) == len(g[prefix + "proj_obj"])
