@@ -199,11 +199,12 @@ void co_tomo_fill(int grid, int n_angles, int n_bins, const double* cos_t, const
 /* A^T as CSR with rows sorted by source row (stable, chunked counting sort) */
 void co_csr_transpose(int64_t m, int64_t n, const int64_t* rp, const int32_t* ci, const float* cv, int64_t* trp,
                       int32_t* tci, float* tcv, int nthreads) {
-  int T = nthreads;
+  /* T fixed row chunks, each handled by one loop iteration: correct whatever
+     team size the runtime grants (chunk t must not depend on thread ids) */
+  int T = nthreads > 0 ? nthreads : 1;
   int64_t* cnt = (int64_t*)calloc((size_t)T * (size_t)n, sizeof(int64_t));
-#pragma omp parallel num_threads(T)
-  {
-    int t = omp_get_thread_num();
+#pragma omp parallel for schedule(static, 1) num_threads(T)
+  for (int t = 0; t < T; ++t) {
     int64_t r0 = m * t / T, r1 = m * (t + 1) / T;
     int64_t* c = cnt + (size_t)t * n;
     for (int64_t p = rp[r0]; p < rp[r1]; ++p) c[ci[p]]++;
@@ -219,9 +220,8 @@ void co_csr_transpose(int64_t m, int64_t n, const int64_t* rp, const int32_t* ci
     }
   }
   trp[n] = run;
-#pragma omp parallel num_threads(T)
-  {
-    int t = omp_get_thread_num();
+#pragma omp parallel for schedule(static, 1) num_threads(T)
+  for (int t = 0; t < T; ++t) {
     int64_t r0 = m * t / T, r1 = m * (t + 1) / T;
     int64_t* c = cnt + (size_t)t * n;
     for (int64_t r = r0; r < r1; ++r)
