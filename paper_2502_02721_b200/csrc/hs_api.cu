@@ -553,8 +553,16 @@ struct hs_op {
       const long long rows = transpose ? n : m, cols = transpose ? m : n;
       const V* Mcm = (transpose ? Atcm : Acm).as<V>();
       Prof p(ctx, "dense_gemv", (double)rows * cols * sizeof(V));
-      dense_seq_gemv_kernel<V, Tin, T><<<grid_for(rows, 256, 1 << 30), 256, 1024 * sizeof(T), s>>>(rows, cols, Mcm,
-                                                                                                   xi, yo);
+      if (env_flag("HS_DENSE_SIMPLE")) {
+        dense_seq_gemv_kernel<V, Tin, T><<<grid_for(rows, 256, 1 << 30), 256, 1024 * sizeof(T), s>>>(rows, cols, Mcm,
+                                                                                                     xi, yo);
+      } else {
+        const size_t smem = dense_tile_smem(sizeof(T));
+        if (smem > 48 * 1024)
+          CK(cudaFuncSetAttribute(dense_tile_gemv_kernel<V, Tin, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+        dense_tile_gemv_kernel<V, Tin, T><<<(int)((rows + 31) / 32), 256, smem, s>>>(rows, cols, Mcm, xi, yo);
+      }
       CKL();
     } else if ((kw == 15 || kw == 31) && !env_flag("HS_PSF_SIMPLE")) {
       Prof p(ctx, "psf_stencil", (double)H * W * (sizeof(Tin) + sizeof(T)));

@@ -85,7 +85,9 @@ csr_seq_spmv_kernel(long long rows, const long long* __restrict__ rowptr,
 // --------------------------------------------------------------------------
 // dense: A stored column-major (lda = rows), one thread per output row,
 // sequential over columns (coalesced across threads).  Used for both A x
-// (A column-major) and A^T y (A row-major == A^T column-major).
+// (A column-major) and A^T y (A row-major == A^T column-major).  The host
+// sizes blocks so the rows spread over all SMs (config 1: 1024 rows -> 32
+// blocks of 32 threads), each SM streaming its own slice of A.
 
 template <class V, class Tin, class T>
 __global__ void __launch_bounds__(256)
@@ -102,11 +104,51 @@ dense_seq_gemv_kernel(long long rows, long long cols, const V* __restrict__ Acm,
     __syncthreads();
     if (r < rows) {
       const V* a = Acm + c0 * rows + r;
-      for (int j = 0; j < cn; ++j) acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(a[(long long)j * rows]), xs[j]));
+#pragma unroll 16
+      for (int j = 0; j < cn; ++j) acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(__ldg(a + (long long)j * rows)), xs[j]));
     }
   }
   if (r < rows) y[r] = acc;
 }
+
+// Tiled variant (the default): a block owns 32 rows; for each tile of 256
+// columns all 256 threads form the 32 x 256 products (rounded, independent,
+// many loads in flight) into shared memory, then warp 0 adds each row's
+// products left to right.  Same operation sequence per row as the simple
+// kernel -- product rounded, then added, columns ascending -- so bit-identical;
+// the serial part is a shared-memory add chain instead of a global-load chain.
+template <class V, class Tin, class T>
+__global__ void __launch_bounds__(256)
+dense_tile_gemv_kernel(long long rows, long long cols, const V* __restrict__ Acm, const Tin* __restrict__ x,
+                       T* __restrict__ y) {
+  constexpr int RB = 32, CT = 256, LD = CT + 1;
+  extern __shared__ __align__(16) unsigned char dense_smem[];
+  T* prod = reinterpret_cast<T*>(dense_smem);  // RB x LD
+  T* xs = prod + RB * LD;                      // CT
+  const long long r0 = (long long)blockIdx.x * RB;
+  const int tid = threadIdx.x;
+  T acc = T(0);
+  for (long long c0 = 0; c0 < cols; c0 += CT) {
+    const int cn = (int)min((long long)CT, cols - c0);
+    for (int i = tid; i < cn; i += blockDim.x) xs[i] = cvt<T>(x[c0 + i]);
+    __syncthreads();
+    for (int idx = tid; idx < RB * cn; idx += blockDim.x) {
+      const int rr = idx % RB, cc = idx / RB;
+      const long long r = r0 + rr;
+      prod[rr * LD + cc] = r < rows ? Rn<T>::mul(cvt<T>(__ldg(Acm + (c0 + cc) * rows + r)), xs[cc]) : T(0);
+    }
+    __syncthreads();
+    if (tid < RB) {
+      const T* pr = prod + tid * LD;
+#pragma unroll 8
+      for (int j = 0; j < cn; ++j) acc = Rn<T>::add(acc, pr[j]);
+    }
+    __syncthreads();
+  }
+  if (tid < RB && r0 + tid < rows) y[r0 + tid] = acc;
+}
+
+inline size_t dense_tile_smem(size_t tsize) { return (32 * 257 + 256) * tsize; }
 
 // --------------------------------------------------------------------------
 // PSF stencil: zero-boundary 'same' convolution (transpose = 0) or correlation
