@@ -42,8 +42,8 @@ __device__ __forceinline__ void gauss_quad(uint2 key, unsigned long long c, unsi
 // result is bit-identical whether it is sketched alone or in a batch.
 // part layout: part[(w * ntiles + tile) * ell + i].
 constexpr int GAUSS_CH = 1024;
-template <class Tin, int NV>
-__global__ void __launch_bounds__(256)
+template <class Tin, int NV, int UNR = 2>
+__global__ void __launch_bounds__(256, 2)
 sketch_gauss_partial_kernel(int ell, long long m, long long col_offset, long long tile_cols, uint2 key,
                             const Tin* __restrict__ v, long long ldv, int nv, double* __restrict__ part) {
   extern __shared__ __align__(128) unsigned char gauss_smem[];
@@ -72,7 +72,7 @@ sketch_gauss_partial_kernel(int ell, long long m, long long col_offset, long lon
     }
     __syncthreads();
     if (active) {
-#pragma unroll 2
+#pragma unroll UNR
       for (int i = ph; i < cn; i += PH) {
         float g[4];
         gauss_quad(key, (unsigned long long)(cb + i + col_offset), (unsigned)q, g);
@@ -128,16 +128,18 @@ constexpr int GAUSS_NV_MAX = 8;
 
 // launch the partial + reduce pair for nv vectors (column stride ldv) into
 // z[w * ldz + i]; batches larger than GAUSS_NV_MAX go in groups
-template <class Tin, int NV>
+template <class Tin, int NV, int UNR = 2>
 inline void gauss_partial_launch(dim3 grid, cudaStream_t s, int ell, long long m, long long col_offset,
                                  long long tile_cols, uint2 key, const Tin* v, long long ldv, int nv, double* part) {
   const size_t smem = (size_t)GAUSS_CH * NV * sizeof(double);
   static bool attr = false;  // per instantiation
   if (!attr && smem > 48 * 1024) {
-    cudaFuncSetAttribute(sketch_gauss_partial_kernel<Tin, NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(sketch_gauss_partial_kernel<Tin, NV, UNR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
     attr = true;
   }
-  sketch_gauss_partial_kernel<Tin, NV><<<grid, 256, smem, s>>>(ell, m, col_offset, tile_cols, key, v, ldv, nv, part);
+  sketch_gauss_partial_kernel<Tin, NV, UNR><<<grid, 256, smem, s>>>(ell, m, col_offset, tile_cols, key, v, ldv, nv,
+                                                                    part);
 }
 
 __global__ void sketch_tile_reduce_kernel(int ell, int ntiles, const double* __restrict__ part, double scale,
