@@ -63,6 +63,44 @@ inline size_t qr_smem_bytes(int Ls, int NB, int kmax) {
   return ((size_t)((Ls + NB - 1) / NB) + 4 * (size_t)kmax) * sizeof(double);
 }
 
+// out[i] = sum_{r < nr} Q[i*ldq + r] * v[r] for i < j: one warp per column,
+// lanes over the rows (then a shuffle sum); four columns per warp pass so
+// their loads are in flight together.  The per-column order is fixed.
+__device__ __forceinline__ void block_dots(const double* __restrict__ Q, int ldq, int j, const double* v, int nr,
+                                           double* __restrict__ out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (int i0 = warp; i0 < j; i0 += 4 * nwarps) {
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int r = lane; r < nr; r += 32) {
+      const double vr = v[r];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * nwarps;
+        if (i < j) s[u] = fma(Q[(long long)i * ldq + r], vr, s[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double t = warp_sum(s[u]);
+      const int i = i0 + u * nwarps;
+      if (lane == 0 && i < j) out[i] = t;
+    }
+  }
+}
+
+__device__ __forceinline__ double block_max(double v, double* scratch) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if (lane == 0) scratch[w] = v;
+  __syncthreads();
+  double r = scratch[0];
+  for (int i = 1; i < nw; ++i) r = fmax(r, scratch[i]);
+  __syncthreads();
+  return r;
+}
+
 __global__ void __launch_bounds__(256) qr_step_kernel(QrArgs a, int k, int iter) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
@@ -92,18 +130,13 @@ __global__ void __launch_bounds__(256) qr_step_kernel(QrArgs a, int k, int iter)
     av[r] = gr < a.ell ? a.zcol[gr] : a.lam * a.fcol[gr - a.ell];
   }
   __syncthreads();
-  for (int i = warp; i < j; i += nwarps) {
-    const double* qi = a.Q + (long long)i * a.ldq + r0;
-    double s = 0.0;
-    for (int r = lane; r < nr; r += 32) s = fma(qi[r], av[r], s);
-    s = warp_sum(s);
-    if (lane == 0) P1[(long long)b * pld + i] = s;
-  }
+  block_dots(a.Q + r0, a.ldq, j, av, nr, P1 + (long long)b * pld);
   grid.sync();
 
   // phase 2: c1 = sum_b P1;  a -= Q c1;  partial Q^T a
   for (int i = tid; i < j; i += BT) {
     double s = 0.0;
+    #pragma unroll 8
     for (int bb = 0; bb < NB; ++bb) s += __ldcg(&P1[(long long)bb * pld + i]);
     cv[i] = s;
     c1s[i] = s;
@@ -111,22 +144,18 @@ __global__ void __launch_bounds__(256) qr_step_kernel(QrArgs a, int k, int iter)
   __syncthreads();
   for (int r = tid; r < nr; r += BT) {
     double s = 0.0;
+    #pragma unroll 8
     for (int i = 0; i < j; ++i) s = fma(a.Q[(long long)i * a.ldq + r0 + r], cv[i], s);
     av[r] -= s;
   }
   __syncthreads();
-  for (int i = warp; i < j; i += nwarps) {
-    const double* qi = a.Q + (long long)i * a.ldq + r0;
-    double s = 0.0;
-    for (int r = lane; r < nr; r += 32) s = fma(qi[r], av[r], s);
-    s = warp_sum(s);
-    if (lane == 0) P2[(long long)b * pld + i] = s;
-  }
+  block_dots(a.Q + r0, a.ldq, j, av, nr, P2 + (long long)b * pld);
   grid.sync();
 
   // phase 3: c2 = sum_b P2;  a -= Q c2;  partial |a|^2 and a^T rhs
   for (int i = tid; i < j; i += BT) {
     double s = 0.0;
+    #pragma unroll 8
     for (int bb = 0; bb < NB; ++bb) s += __ldcg(&P2[(long long)bb * pld + i]);
     cv[i] = s;
   }
@@ -134,6 +163,7 @@ __global__ void __launch_bounds__(256) qr_step_kernel(QrArgs a, int k, int iter)
   double nn = 0.0, ar = 0.0;
   for (int r = tid; r < nr; r += BT) {
     double s = 0.0;
+    #pragma unroll 8
     for (int i = 0; i < j; ++i) s = fma(a.Q[(long long)i * a.ldq + r0 + r], cv[i], s);
     const double v = av[r] - s;
     av[r] = v;
@@ -151,13 +181,16 @@ __global__ void __launch_bounds__(256) qr_step_kernel(QrArgs a, int k, int iter)
 
   // phase 4: rho, beta; new Q column; block 0 updates R^{-1}, y
   double rho2 = 0.0, g = 0.0;
+#pragma unroll 8
   for (int bb = 0; bb < NB; ++bb) {
     rho2 += __ldcg(&P3[(long long)bb * pld + 0]);
     g += __ldcg(&P3[(long long)bb * pld + 1]);
   }
   const double rho = sqrt(rho2);
-  double rmax = rho;
-  for (int i = 0; i < j; ++i) rmax = fmax(rmax, fabs(a.Rdiag[i]));
+  // max |R_ii| (order-free): strided partial maxima, block reduction
+  double rmax = 0.0;
+  for (int i = tid; i < j; i += BT) rmax = fmax(rmax, fabs(a.Rdiag[i]));
+  rmax = fmax(rho, block_max(rmax, scratch));
   const bool deficient = !(rho > 0.0) || rho < 1e-14 * rmax;
   for (int r = tid; r < nr; r += BT) a.Q[(long long)j * a.ldq + r0 + r] = deficient ? 0.0 : av[r] / rho;
   if (b == 0) {
@@ -165,6 +198,7 @@ __global__ void __launch_bounds__(256) qr_step_kernel(QrArgs a, int k, int iter)
     // w = Rinv[0:j, 0:j] (c1 + c2)
     for (int i = tid; i < j; i += BT) {
       double s = 0.0;
+      #pragma unroll 8
       for (int l = i; l < j; ++l) s = fma(a.Rinv[(long long)l * a.kmax + i], c1s[l] + cv[l], s);
       const double yi = a.y[i] - eta * s;
       a.Rinv[(long long)j * a.kmax + i] = deficient ? 0.0 : -s / rho;
@@ -240,12 +274,14 @@ __global__ void __launch_bounds__(256) qr_step_kernel(QrArgs a, int k, int iter)
     const int gr = r0 + r;
     if (gr < a.ell) {
       double s = 0.0;
+      #pragma unroll 8
       for (int i = 0; i <= j; ++i) s = fma(a.Z[(long long)i * a.ell + gr], ys[i], s);
       const double d = s - a.sr0[gr];
       s_top = fma(d, d, s_top);
     } else {
       const int fr = gr - a.ell;
       double s = 0.0;
+      #pragma unroll 8
       for (int i = 0; i <= j; ++i) s = fma(a.F[(long long)i * a.ell + fr], ys[i], s);
       s_bot = fma(s, s, s_bot);
     }
