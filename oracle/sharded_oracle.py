@@ -157,3 +157,81 @@ def sharded_slslu(K, b, S2, maxiter, grid, n_angles, n_bins, dtype=np.float32, x
         W[: j + 1, j] = col
     return dict(t=np.array(t), g=np.array(g), H=H, W=W, x=x, D_loc=np.column_stack(D), L_loc=np.column_stack(L),
                 plan=pl, k=kend)
+
+
+def _halo_window(own, rows, width, ry, rank, ws):
+    """Own image rows plus ry halo rows from each neighbour (zero outside the
+    image), exchanged point to point like hs_dist.inc:halo_exchange."""
+    own = np.asarray(own).reshape(rows, width)
+    assert ws == 1 or rows >= ry, "shards thinner than the halo are rejected (hs_op_psf_create)"
+    win = np.zeros((rows + 2 * ry, width), dtype=own.dtype)
+    win[ry : ry + rows] = own
+    reqs = []
+    if rank > 0:
+        reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(own[:ry], dtype=np.float64)), rank - 1))
+    if rank < ws - 1:
+        reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(own[rows - ry :], dtype=np.float64)), rank + 1))
+    if rank > 0:
+        t = torch.zeros((ry, width), dtype=torch.float64)
+        dist.recv(t, rank - 1)
+        win[:ry] = t.numpy().astype(own.dtype)
+    if rank < ws - 1:
+        t = torch.zeros((ry, width), dtype=torch.float64)
+        dist.recv(t, rank + 1)
+        win[ry + rows :] = t.numpy().astype(own.dtype)
+    for r in reqs:
+        r.wait()
+    return win
+
+
+def sharded_scmrh_psf(psf, b, S2, maxiter, shape, dtype=np.float32, stencil=None):
+    """Row-sharded sCMRH on the PSF operator (hs_dist.inc:run_square): rank r
+    owns image rows [row0, row0 + rows); each operator application is the
+    tap-ordered stencil on the window (own rows + halos) restricted to the own
+    rows.  Returns the global pivots, H, x and the rank-local basis shard."""
+    from paper_2502_02721_b200.dist import psf_shard_plan
+
+    dt = np.dtype(dtype)
+    ws, rank = dist.get_world_size(), dist.get_rank()
+    Hh, Ww = shape
+    n = Hh * Ww
+    ry = psf.shape[0] // 2
+    pl = psf_shard_plan(Hh, Ww, ws, rank)
+    rows = pl.n_loc // Ww
+    S2_loc = np.asarray(S2)[:, pl.n_off : pl.n_off + pl.n_loc]
+
+    def A_loc(v_loc):
+        win = _halo_window(v_loc, rows, Ww, ry, rank, ws)
+        return stencil(win, psf, False, dt)[ry : ry + rows].ravel()
+
+    r0 = np.asarray(b[pl.n_off : pl.n_off + pl.n_loc], dtype=dt)
+    best = _merge(_gather_objects(_local_best(r0, pl.n_off)))
+    beta = dt.type(best[1])
+    t = [best[2]]
+    L = [r0 / beta]
+    PL = [[dt.type(1)]]
+    sr0 = _allreduce(S2_loc @ r0.astype(np.float64))
+    Z, h_cols = [], []
+    for k in range(1, maxiter + 1):
+        u = A_loc(L[-1])
+        Z.append(_allreduce(S2_loc @ u.astype(np.float64)))
+        c = _coefficients(_owner_values(u, pl.n_off, pl.n_loc, pl.n_blk, t[:k]), PL, dt)
+        for j in range(k):
+            u = u - c[j] * L[j]
+        best = _merge(_gather_objects(_local_best(u, pl.n_off)))
+        val = dt.type(best[1]) if k < n else dt.type(0)
+        h_cols.append(np.array([float(x_) for x_ in c] + [float(val)]))
+        if val == 0:
+            break
+        t.append(best[2])
+        PL.append([dt.type(_owner_values(L[i], pl.n_off, pl.n_loc, pl.n_blk, [best[2]])[0]) for i in range(k)]
+                  + [dt.type(1)])
+        L.append(u / val)
+    kend = len(h_cols)
+    y = ho.dense_qr_ls(np.column_stack(Z), sr0)
+    xl = np.column_stack(L[:kend]).astype(np.float64) @ y
+    x = _allgather(xl, pl.n_blk)[:n]
+    H = np.zeros((kend + 1, kend))
+    for j, col in enumerate(h_cols):
+        H[: j + 2, j] = col
+    return dict(t=np.array(t), H=H, x=x, L_loc=np.column_stack(L), plan=pl, k=kend)

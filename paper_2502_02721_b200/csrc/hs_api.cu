@@ -475,6 +475,9 @@ struct hs_op {
   // psf
   int H = 0, W = 0, kh = 0, kw = 0;
   DBuf K;
+  // sharded psf: this rank's image rows [psf_row0, psf_row0 + psf_rows); window scratch
+  long long psf_row0 = 0, psf_rows = 0;
+  mutable DBuf psfwin;
 
   template <class V, class Tin, class T>
   void apply_t(const void* x, void* y, bool transpose) const {
@@ -564,32 +567,77 @@ struct hs_op {
         dense_tile_gemv_kernel<V, Tin, T><<<(int)((rows + 31) / 32), 256, smem, s>>>(rows, cols, Mcm, xi, yo);
       }
       CKL();
-    } else if ((kw == 15 || kw == 31) && !env_flag("HS_PSF_SIMPLE")) {
-      Prof p(ctx, "psf_stencil", (double)H * W * (sizeof(Tin) + sizeof(T)));
+    } else if (kind == OP_PSF && sharded) {
+      // x is the full image (all ranks' rows): cut this rank's window (own
+      // rows + kh/2 halo rows each side, zero outside the image)
+      const int ry = kh / 2;
+      const long long win_rows = psf_rows + 2LL * ry;
+      const size_t need = (size_t)win_rows * W * sizeof(Tin);
+      if (psfwin.bytes < need) psfwin.alloc(need, false);
+      CK(cudaMemsetAsync(psfwin.p, 0, need, s));
+      const long long g0 = std::max<long long>(0, psf_row0 - ry), g1 = std::min<long long>(H, psf_row0 + psf_rows + ry);
+      CK(cudaMemcpyAsync(psfwin.as<Tin>() + (g0 - (psf_row0 - ry)) * W, xi + g0 * W, (size_t)(g1 - g0) * W * sizeof(Tin),
+                         cudaMemcpyDeviceToDevice, s));
+      psf_launch<V, Tin, T>(psfwin.as<Tin>(), (int)win_rows, ry, (int)psf_rows, yo, transpose);
+    } else {
+      psf_launch<V, Tin, T>(xi, H, 0, H, yo, transpose);
+    }
+  }
+
+  // PSF stencil on an x of `rows` image rows (width W), output rows
+  // [out_row0, out_row0 + out_rows) into y (row out_row0 first)
+  template <class V, class Tin, class T>
+  void psf_launch(const Tin* xi, int rows, int out_row0, int out_rows, T* yo, bool transpose) const {
+    cudaStream_t s = ctx->stream;
+    Prof p(ctx, "psf_stencil", (double)out_rows * W * (sizeof(Tin) + sizeof(T)));
+    if ((kw == 15 || kw == 31) && !env_flag("HS_PSF_SIMPLE")) {
       auto launch = [&](auto kwc) {
         constexpr int KWc = decltype(kwc)::value;
         using G = PsfRb<T, KWc>;
-        const dim3 grid((W + G::TILE_X - 1) / G::TILE_X, (H + G::TY - 1) / G::TY);
+        const dim3 grid((W + G::TILE_X - 1) / G::TILE_X, (out_rows + G::TY - 1) / G::TY);
         const size_t smem = G::smem(kh);
         auto kern = transpose ? psf_stencil_rb_kernel<V, Tin, T, KWc, G::R, G::TXT, G::TY, true>
                               : psf_stencil_rb_kernel<V, Tin, T, KWc, G::R, G::TXT, G::TY, false>;
         if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kern<<<grid, G::TXT * G::TY, smem, s>>>(H, W, kh, K.as<V>(), xi, yo);
+        kern<<<grid, G::TXT * G::TY, smem, s>>>(rows, W, kh, K.as<V>(), xi, yo, out_row0, out_rows);
         CKL();
       };
       if (kw == 15) launch(std::integral_constant<int, 15>());
       else launch(std::integral_constant<int, 31>());
     } else {
       constexpr int TX = 32, TY = 8;
-      dim3 grid((W + TX - 1) / TX, (H + TY - 1) / TY);
+      dim3 grid((W + TX - 1) / TX, (out_rows + TY - 1) / TY);
       const size_t smem = ((size_t)(TX + 2 * (kw / 2)) * (TY + 2 * (kh / 2)) + (size_t)kh * kw) * sizeof(T);
-      Prof p(ctx, "psf_stencil", (double)H * W * (sizeof(Tin) + sizeof(T)));
       if (smem > 48 * 1024)
         CK(cudaFuncSetAttribute(psf_stencil_kernel<V, Tin, T, TX, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
-      psf_stencil_kernel<V, Tin, T, TX, TY><<<grid, TX * TY, smem, s>>>(H, W, kh, kw, K.as<V>(), xi, yo,
-                                                                         transpose ? 1 : 0);
+      psf_stencil_kernel<V, Tin, T, TX, TY><<<grid, TX * TY, smem, s>>>(rows, W, kh, kw, K.as<V>(), xi, yo,
+                                                                         transpose ? 1 : 0, out_row0, out_rows);
       CKL();
+    }
+  }
+
+  // sharded PSF: stencil of this rank's rows from a prepared window (own rows
+  // + halos, `win_rows` = psf_rows + 2 * (kh / 2) rows, type xdt) into y (wdt)
+  void apply_psf_window(const void* win, int xdt, void* y, int wdt, bool transpose) const {
+    const int ry = kh / 2;
+    auto go = [&](auto vt, auto it, auto ot) {
+      using V = decltype(vt);
+      using Tin = decltype(it);
+      using T = decltype(ot);
+      psf_launch<V, Tin, T>(reinterpret_cast<const Tin*>(win), (int)(psf_rows + 2 * ry), ry, (int)psf_rows,
+                            reinterpret_cast<T*>(y), transpose);
+    };
+    if (wdt == HS_F64) {
+      if (xdt != HS_F64) fail(HS_ERR_TYPE, "fp64 work needs fp64 input vectors");
+      if (vdtype == HS_F64) go(double{}, double{}, double{});
+      else go(float{}, double{}, double{});
+    } else if (xdt == HS_F32) {
+      if (vdtype == HS_F64) go(double{}, float{}, float{});
+      else go(float{}, float{}, float{});
+    } else {
+      if (vdtype == HS_F64) go(double{}, __nv_bfloat16{}, float{});
+      else go(float{}, __nv_bfloat16{}, float{});
     }
   }
 

@@ -155,17 +155,20 @@ inline size_t dense_tile_smem(size_t tsize) { return (32 * 257 + 256) * tsize; }
 // (transpose = 1) on an H x W image, taps summed a-major / b-minor
 // (oracle/tomo_oracle.py:psf_stencil), smem-tiled with the zero halo.
 
+// Output rows [out_row0, out_row0 + out_rows) of the H-row image x are written
+// to y[(r - out_row0) * W + c] (a row-sharded rank passes its rows plus the
+// neighbours' halo rows as x and computes only its own rows).
 template <class V, class Tin, class T, int TILE_X, int TILE_Y>
 __global__ void __launch_bounds__(TILE_X * TILE_Y)
 psf_stencil_kernel(int H, int W, int kh, int kw, const V* __restrict__ K,
-                   const Tin* __restrict__ x, T* __restrict__ y, int transpose) {
+                   const Tin* __restrict__ x, T* __restrict__ y, int transpose, int out_row0, int out_rows) {
   extern __shared__ unsigned char smem_raw[];
   const int ry = kh / 2, rx = kw / 2;
   const int SW = TILE_X + 2 * rx, SH = TILE_Y + 2 * ry;
   T* tile = reinterpret_cast<T*>(smem_raw);
   T* ks = tile + SW * SH;
   const int tx = threadIdx.x % TILE_X, ty = threadIdx.x / TILE_X;
-  const int c0 = blockIdx.x * TILE_X, r0 = blockIdx.y * TILE_Y;
+  const int c0 = blockIdx.x * TILE_X, r0 = out_row0 + blockIdx.y * TILE_Y;
   for (int i = threadIdx.x; i < kh * kw; i += blockDim.x) ks[i] = cvt<T>(K[i]);
   for (int i = threadIdx.x; i < SW * SH; i += blockDim.x) {
     const int sr = i / SW, sc = i % SW;
@@ -176,7 +179,7 @@ psf_stencil_kernel(int H, int W, int kh, int kw, const V* __restrict__ K,
   }
   __syncthreads();
   const int r = r0 + ty, c = c0 + tx;
-  if (r >= H || c >= W) return;
+  if (r >= out_row0 + out_rows || c >= W) return;
   T acc = T(0);
   if (!transpose) {
     // out[r,c] = sum_a sum_b K[a,b] x[r + ry - a, c + rx - b]
@@ -193,7 +196,7 @@ psf_stencil_kernel(int H, int W, int kh, int kw, const V* __restrict__ K,
       for (int b = 0; b < kw; ++b) acc = Rn<T>::add(acc, Rn<T>::mul(krow[b], trow[b]));
     }
   }
-  y[(long long)r * W + c] = acc;
+  y[(long long)(r - out_row0) * W + c] = acc;
 }
 
 // Register-blocked variant for the common odd widths (KW = 15, 31): each
@@ -205,7 +208,7 @@ psf_stencil_kernel(int H, int W, int kh, int kw, const V* __restrict__ K,
 template <class V, class Tin, class T, int KW, int R, int TXT, int TY, bool TR>
 __global__ void __launch_bounds__(TXT * TY)
 psf_stencil_rb_kernel(int H, int W, int kh, const V* __restrict__ K, const Tin* __restrict__ x,
-                      T* __restrict__ y) {
+                      T* __restrict__ y, int out_row0, int out_rows) {
   constexpr int rx = KW / 2;
   constexpr int TILE_X = TXT * R;
   constexpr int SW = ((TILE_X + 2 * rx + 3) / 4) * 4;  // row pitch (16-byte aligned rows)
@@ -216,7 +219,7 @@ psf_stencil_rb_kernel(int H, int W, int kh, const V* __restrict__ K, const Tin* 
   T* tile = reinterpret_cast<T*>(smem_raw);
   T* ks = tile + SW * SH;
   const int tx = threadIdx.x % TXT, ty = threadIdx.x / TXT;
-  const int c0 = blockIdx.x * TILE_X, r0 = blockIdx.y * TY;
+  const int c0 = blockIdx.x * TILE_X, r0 = out_row0 + blockIdx.y * TY;
   for (int i = threadIdx.x; i < kh * KW; i += blockDim.x) ks[i] = cvt<T>(K[i]);
   for (int i = threadIdx.x; i < SW * SH; i += blockDim.x) {
     const int sr = i / SW, sc = i - sr * SW;
@@ -227,7 +230,7 @@ psf_stencil_rb_kernel(int H, int W, int kh, const V* __restrict__ K, const Tin* 
   }
   __syncthreads();
   const int r = r0 + ty, cb = c0 + tx * R;
-  if (r >= H || cb >= W) return;
+  if (r >= out_row0 + out_rows || cb >= W) return;
   T acc[R];
 #pragma unroll
   for (int j = 0; j < R; ++j) acc[j] = T(0);
@@ -244,7 +247,7 @@ psf_stencil_rb_kernel(int H, int W, int kh, const V* __restrict__ K, const Tin* 
       for (int j = 0; j < R; ++j) acc[j] = Rn<T>::add(acc[j], Rn<T>::mul(kab, w[TR ? j + b : j + KW - 1 - b]));
     }
   }
-  T* yr = y + (long long)r * W + cb;
+  T* yr = y + (long long)(r - out_row0) * W + cb;
 #pragma unroll
   for (int j = 0; j < R; ++j)
     if (cb + j < W) yr[j] = acc[j];

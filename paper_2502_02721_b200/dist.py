@@ -23,7 +23,7 @@ from dataclasses import dataclass
 
 from . import _lib
 
-__all__ = ["ShardPlan", "shard_plan", "init_comm", "comm_info"]
+__all__ = ["ShardPlan", "shard_plan", "psf_shard_plan", "init_comm", "comm_info"]
 
 
 def _round_up(a, b):
@@ -52,6 +52,18 @@ def shard_plan(grid, n_angles, n_bins, nranks, rank):
     n_off = rank * n_blk
     n_loc = max(0, min(n_blk, n - n_off))
     return ShardPlan(m_off, m_loc, m_blk, n_off, n_loc, n_blk)
+
+
+def psf_shard_plan(height, width, nranks, rank):
+    """Image-row blocks of the row-sharded PSF operator (hs_abi.inc:
+    hs_op_psf_create): rank ``rank`` owns rows [row0, row0 + rows) -- entries
+    [off, off + loc) of every n-vector -- and exchanges kh/2 halo rows with each
+    neighbour per operator application."""
+    rows_pr = _round_up(-(-height // nranks), 8)
+    row0 = rank * rows_pr
+    rows = max(0, min(rows_pr, height - row0))
+    blk = rows_pr * width
+    return ShardPlan(row0 * width, rows * width, blk, row0 * width, rows * width, blk)
 
 
 def init_comm(ctx=None):

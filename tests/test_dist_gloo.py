@@ -92,3 +92,55 @@ def test_shard_plan_covers_every_index():
             for r, p in enumerate(plans):
                 assert p.m_off == r * p.m_blk and p.n_off == r * p.n_blk
                 assert p.m_blk % 64 == 0 and p.n_blk % (8 * grid) == 0
+
+
+def _psf_worker(rank, ws, port, cfg, outdir):
+    import torch.distributed as dist
+
+    from oracle import sharded_oracle as so
+    from oracle import tomo_oracle as to
+    from paper_2502_02721_b200.problems import add_noise, gaussian_psf, rectangles_and_discs
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    (Hh, Ww), K, dt = cfg
+    psf = gaussian_psf(2.0, radius=7)
+    x = rectangles_and_discs(max(Hh, Ww), 20, 0)[:Hh, :Ww].ravel()
+    b, _ = add_noise(to.psf_stencil(x.reshape(Hh, Ww), psf, False, np.float64).ravel(), 0.01, 1)
+    S2 = np.random.default_rng(4).standard_normal((4 * K, Hh * Ww)) / np.sqrt(4 * K)
+    out = so.sharded_scmrh_psf(psf, b, S2, K, (Hh, Ww), dtype=dt, stencil=to.psf_stencil)
+    np.savez(os.path.join(outdir, f"psf{rank}.npz"), t=out["t"], H=out["H"], x=out["x"], L=out["L_loc"])
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("ws,shape", [(2, (40, 37)), (3, (60, 24))])
+def test_sharded_psf_model_matches_single_process(tmp_path, ws, shape):
+    """Row-sharded sCMRH on the PSF operator with halo exchange (hs_dist.inc:
+    run_square): pivots, H and the basis shards bit-identical to the single
+    process for 2 and 3 ranks (uneven last shard)."""
+    from oracle import hessketch_oracle as ho
+    from oracle import tomo_oracle as to
+    from paper_2502_02721_b200.dist import psf_shard_plan
+    from paper_2502_02721_b200.problems import add_noise, gaussian_psf, rectangles_and_discs
+
+    K, dt = 14, np.float32
+    Hh, Ww = shape
+    mp.spawn(_psf_worker, args=(ws, _free_port(), (shape, K, dt), str(tmp_path)), nprocs=ws, join=True)
+    psf = gaussian_psf(2.0, radius=7)
+    x = rectangles_and_discs(max(Hh, Ww), 20, 0)[:Hh, :Ww].ravel()
+    b, _ = add_noise(to.psf_stencil(x.reshape(Hh, Ww), psf, False, np.float64).ravel(), 0.01, 1)
+    S2 = np.random.default_rng(4).standard_normal((4 * K, Hh * Ww)) / np.sqrt(4 * K)
+    A = ho.Operator(Hh * Ww, Hh * Ww,
+                    lambda v: to.psf_stencil(v.reshape(Hh, Ww), psf, False, dt).ravel(),
+                    lambda v: to.psf_stencil(v.reshape(Hh, Ww), psf, True, dt).ravel(), dt)
+    ref = ho.hessenberg_solve(A, b, square=True, maxiter=K, S2=S2)
+    t_ref, _ = ho.pivots_of(ref.state)
+    L_ref = np.column_stack(ref.state.L)
+    for r in range(ws):
+        got = dict(np.load(tmp_path / f"psf{r}.npz"))
+        np.testing.assert_array_equal(got["t"], t_ref)
+        np.testing.assert_array_equal(got["H"], ref.state.H_matrix())
+        pl = psf_shard_plan(Hh, Ww, ws, r)
+        np.testing.assert_array_equal(got["L"], L_ref[pl.n_off:pl.n_off + pl.n_loc])
+        np.testing.assert_allclose(got["x"], ref.x, rtol=1e-9, atol=1e-12 * np.abs(ref.x).max())

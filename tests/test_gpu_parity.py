@@ -673,3 +673,45 @@ def test_sharded_path_single_rank(hs, lam, basis):
     # (fp32-accumulated) one -- equal to rounding, not bitwise
     np.testing.assert_allclose(r2.trace.column("rel_err"), r1.trace.column("rel_err"), rtol=1e-6)
     assert r2.trace.column("sketches") == r1.trace.column("sketches")
+
+
+@pytest.mark.parametrize("sigma,radius,size,basis,lam", [(2.0, 7, 64, "float32", 0.0), (4.0, 15, 96, "bfloat16", 0.0),
+                                                         (2.0, 7, 72, "float32", 0.05)])
+def test_sharded_psf_single_rank(hs, sigma, radius, size, basis, lam):
+    """The row-sharded PSF operator (window + halo exchange) and the sharded
+    sCMRH loop (hs_dist.inc:run_square) forced on one rank reproduce the
+    single-GPU path: operator bit for bit; pivots, H, basis, sketches, y and x
+    bit for bit; rel_err to rounding (the iterate is fused at a different lag)."""
+    from paper_2502_02721_b200 import dist as hsd
+    from paper_2502_02721_b200.problems import add_noise, gaussian_psf, rectangles_and_discs
+
+    K = 30
+    psf = gaussian_psf(sigma, radius=radius)
+    x = rectangles_and_discs(size, 20, 0).ravel()
+    op1 = hs.PsfOperator(size, psf, dtype=np.float32)
+    b, _ = add_noise(op1.matvec(x), 0.01, 1)
+    cfg = hs.SolverConfig(maxiter=K, sketch_rows=4 * K, dtype="float32", basis_dtype=basis, sketch_kind="gaussian",
+                          lam=lam)
+    solve = hs.scmrh_tikhonov if lam > 0 else hs.scmrh
+    r1 = solve(op1, b, cfg, x_true=x)
+    img = np.random.default_rng(2).standard_normal(size * size)
+    hsd.force_sharding(True)
+    try:
+        op2 = hs.PsfOperator(size, psf, dtype=np.float32)
+        for dt in (np.float32, np.float64):
+            np.testing.assert_array_equal(op2.matvec(img.astype(dt), dt), op1.matvec(img.astype(dt), dt))
+            np.testing.assert_array_equal(op2.rmatvec(img.astype(dt), dt), op1.rmatvec(img.astype(dt), dt))
+        r2 = solve(op2, b, cfg, x_true=x)
+    finally:
+        hsd.force_sharding(False)
+    f1, f2 = r1.factorization, r2.factorization
+    assert r1.termination == r2.termination
+    np.testing.assert_array_equal(f2.t[: K + 1], f1.t[: K + 1])
+    np.testing.assert_array_equal(f2.H_matrix(), f1.H_matrix())
+    np.testing.assert_array_equal(f2.L_matrix(), f1.L_matrix())
+    np.testing.assert_array_equal(f2._res.Z, f1._res.Z)
+    np.testing.assert_array_equal(r2.x, r1.x)
+    assert r2.trace.column("sres_norm") == r1.trace.column("sres_norm")
+    assert r2.trace.column("sketches") == r1.trace.column("sketches")
+    assert r2.trace.column("matvecs") == r1.trace.column("matvecs")
+    np.testing.assert_allclose(r2.trace.column("rel_err"), r1.trace.column("rel_err"), rtol=1e-6)
