@@ -88,6 +88,9 @@ typedef struct {
                             residual |b - A x_k| (hs_result_resnorm); Hessenberg
                             solvers also kappa_basis, kappa_dbar, eps_embed
                             (hs_result_diagnostics); serialises the loop      */
+  int32_t printed_f;     /* slslu_tikhonov(printed_f_columns=True) comparison
+                            variant: penalty columns S1 (A^T d_{k+1}) before the
+                            elimination (solvers.py:460-461, 488-490)          */
 } hs_config;
 
 const char* hs_last_error(void);

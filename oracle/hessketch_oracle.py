@@ -489,7 +489,7 @@ class Result:
 
 def hessenberg_solve(
     A, b, *, square, maxiter, ell=None, lam=0.0, seed=0, S2=None, S1=None,
-    x0=None, x_true=None, sketch_basis=False, sketched=True, pivot_sample=0, pivot_seed=0,
+    x0=None, x_true=None, sketch_basis=False, sketched=True, pivot_sample=0, pivot_seed=0, printed_f=False,
 ):
     """Restates ``_hessenberg_solve`` (solvers.py:410-539) for the sketched
     solvers ``scmrh`` / ``slslu`` / ``*_tikhonov`` (solvers.py:562-605) and,
@@ -537,7 +537,10 @@ def hessenberg_solve(
     if lam > 0.0:
         if S1 is None:
             S1 = gaussian_sketch_entries(ell, A.cols, derive_seed(seed, 1))
-        F_cols.append(sketch_apply(S1, state.L[0], c))
+        # printed_f: slslu_tikhonov(printed_f_columns=True) sketches the
+        # unreduced transpose products (solvers.py:460-461, 488-490)
+        f0 = state.last_solution_product if (printed_f and not square) else state.L[0]
+        F_cols.append(sketch_apply(S1, f0, c))
 
     records = []
     termination = "maxiter"
@@ -560,8 +563,12 @@ def hessenberg_solve(
             cols = state.L if square else state.D
             if len(cols) > n_basis_before:
                 G_cols.append(sketch_apply(S2, cols[-1], c))
-        if lam > 0.0 and len(state.L) > n_sol_before:
-            F_cols.append(sketch_apply(S1, state.L[-1], c))
+        if lam > 0.0:
+            if printed_f and not square:
+                if len(state.D) > n_basis_before:
+                    F_cols.append(sketch_apply(S1, state.last_solution_product, c))
+            elif len(state.L) > n_sol_before:
+                F_cols.append(sketch_apply(S1, state.L[-1], c))
 
         Lk = np.column_stack(state.L[:k]).astype(np.float64)
         if sketch_basis:

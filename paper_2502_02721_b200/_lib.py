@@ -44,6 +44,7 @@ class HsConfig(ctypes.Structure):
         ("pivot_sample", ctypes.c_int32),
         ("pivot_positions", ctypes.c_void_p),
         ("diagnostics", ctypes.c_int32),
+        ("printed_f", ctypes.c_int32),
     ]
 
 

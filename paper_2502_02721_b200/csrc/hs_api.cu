@@ -951,6 +951,7 @@ struct Solver {
     const long long ell = skd ? S2->ell : (long long)K + 1;
     const bool lamon = cfg.lam > 0.0;
     const bool sb = cfg.sketch_basis != 0;
+    const bool printed = cfg.printed_f != 0 && !square && lamon && skd;  // slslu_tikhonov(printed_f_columns=True)
     const long long ldm = round_up(m, 64), ldn = round_up(n, 64);
     const int ldp = K + 2;
     const int Ls = (int)(lamon ? 2 * ell : ell);
@@ -1163,7 +1164,9 @@ struct Solver {
         sk0++;
       }
       if (lamon) {
-        S1->apply(Lcol(0), bdt, Fb.as<double>());
+        // printed variant: the unreduced r = A^T d1 still in q (solvers.py:460-461)
+        if (printed) S1->apply(q.p, wdt, Fb.as<double>());
+        else S1->apply(Lcol(0), bdt, Fb.as<double>());
         sk0++;
       }
     } else {
@@ -1280,7 +1283,7 @@ struct Solver {
       const long long slot0 = (long long)((kb0 - 1) % (2 * SB));
       S2->apply_many(uring.as<T>() + slot0 * ldm, wdt, ldm, nb, Zb.as<double>() + (long long)(kb0 - 1) * ell, ell, s2);
       CK(cudaEventRecord(ev_skb[bidx], s2));
-      if (lamon) S1->apply_many(Lcol(kb0), bdt, ldn, nb, Fb.as<double>() + (long long)kb0 * ell, ell, s2);
+      if (lamon && !printed) S1->apply_many(Lcol(kb0), bdt, ldn, nb, Fb.as<double>() + (long long)kb0 * ell, ell, s2);
       for (int kk = kb0; kk <= kend_b; ++kk) {
         qa.zcol = Zb.as<double>() + (long long)(kk - 1) * ell;
         qa.fcol = lamon ? Fb.as<double>() + (long long)(kk - 1) * ell : nullptr;
@@ -1357,6 +1360,8 @@ struct Solver {
         CKL();
         if (sb) S2->apply(Dcol(k), bdt, Gb.as<double>() + (long long)k * ell);
         op->apply(Dcol(k), bdt, q.p, wdt, true);
+        // printed variant: F column k = S1 q before the elimination (solvers.py:488-490)
+        if (printed) S1->apply(q.p, wdt, Fb.as<double>() + (long long)k * ell);
         fsub(q.as<T>(), gpos.as<long long>(), PL.as<T>(), ldp, k, k, 1, cvec.as<T>(), Wcol(k));
         wait_y();
         elim(q.as<T>(), n, ldn, L, k, 1, k, kx, yprev, relslot, q.as<T>());
@@ -1447,7 +1452,7 @@ struct Solver {
       }
       if (SB > 1) {
         if (k % SB == 0) flush_batch(k);
-      } else if (lamon) {
+      } else if (lamon && !printed) {
         // F column k = S1 l_{k+1} (used by the projected solve of iteration k+1)
         if (ovl) {
           CK(cudaEventRecord(ev_l, s));
@@ -1595,7 +1600,7 @@ struct Solver {
       if (!square && grewD) tm += 1;              // q = A^T d_{k+1}
       if (skd) {
         sk += sb ? (grewD ? 1 : 0) : 1;           // G or Z column
-        if (lamon && grewL) sk += 1;              // F column
+        if (lamon && (printed ? grewD : grewL)) sk += 1;  // F column
       }
       res->matvecs[k - 1] = matvec0 + k;
       res->tmatvecs[k - 1] = tm;

@@ -30,7 +30,9 @@ basis condition number ``kappa_basis`` and, with lam > 0, ``kappa_dbar``
 bases + Jacobi SVD of the small R factors), and the measured embedding
 distortion ``eps_embed`` of S2 on span[A l_1..A l_k, r0] (sketch.py:91-112;
 not for ``sketch_basis=True``).  The loop is serialised while diagnostics are
-on.  Out of scope (raises NotImplementedError): ``printed_f_columns=True``.
+on.  ``slslu_tikhonov(..., printed_f_columns=True)`` runs the reference's
+comparison variant (penalty columns from the unreduced A^T d_{k+1},
+solvers.py:460-461, 488-490) on the device too.
 """
 
 from __future__ import annotations
@@ -275,7 +277,8 @@ def pivot_positions(strategy, maxiter, rows, cols, square):
     return out
 
 
-def _hessenberg_solve(A, b, cfg, x_true, square, sketch_basis, sketch=None, S1=None, sketched=True):
+def _hessenberg_solve(A, b, cfg, x_true, square, sketch_basis, sketch=None, S1=None, sketched=True,
+                      printed_f=False):
     """solvers.py:410-539 on the device (sketched or unsketched branch)."""
     cfg = cfg or SolverConfig()
     if square and not A.is_square:
@@ -325,6 +328,7 @@ def _hessenberg_solve(A, b, cfg, x_true, square, sketch_basis, sketch=None, S1=N
         sketched=1 if sketched else 0, pivot_sample=0 if positions is None else int(cfg.pivot.sample_size),
         pivot_positions=None if positions is None else positions.ctypes.data,
         diagnostics=1 if cfg.compute_diagnostics else 0,
+        printed_f=1 if printed_f else 0,
     )
     h = _lib.c_vp()
     _lib.check(_lib.load().hs_solve(dev.ctx.handle, dev.handle, ctypes.byref(hc),
@@ -372,9 +376,7 @@ def scmrh_tikhonov(A, b, cfg=None, x_true=None):
 
 def slslu_tikhonov(A, b, cfg=None, x_true=None, *, printed_f_columns=False):
     """slslu with the sketched penalty (solvers.py:594-605)."""
-    if printed_f_columns:
-        raise NotImplementedError("the printed-F comparison variant is out of scope")
-    return _hessenberg_solve(A, b, cfg, x_true, False, False)
+    return _hessenberg_solve(A, b, cfg, x_true, False, False, printed_f=bool(printed_f_columns))
 
 
 def _krylov_solve(A, b, cfg, x_true, method):

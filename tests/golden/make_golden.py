@@ -470,6 +470,21 @@ def gen_rank_fallback():
     _save("rank_fallback", **o)
 
 
+def gen_printed_f():
+    """slslu_tikhonov(printed_f_columns=True): penalty columns from the
+    unreduced A^T d_{k+1} (solvers.py:460-461, 488-490, 594-605)."""
+    rng = np.random.default_rng(11)
+    M = rng.standard_normal((31, 24))
+    b = rng.standard_normal(31)
+    xt = rng.standard_normal(24)
+    A = LinearOperator.from_matrix(M)
+    o = dict(M=M, b=b, xt=xt)
+    cfg = solvers.SolverConfig(maxiter=8, seed=6, lam=0.5)
+    o.update(_pack_result(solvers.slslu_tikhonov(A, b, cfg, x_true=xt, printed_f_columns=True), "pr_"))
+    o.update(_pack_result(solvers.slslu_tikhonov(A, b, cfg, x_true=xt), "df_"))
+    _save("printed_f", **o)
+
+
 if __name__ == "__main__":
     print("reference hessketch", hessketch.__version__)
     if len(sys.argv) > 1:  # regenerate selected fixtures only: make_golden.py gen_rank_fallback ...
@@ -487,3 +502,4 @@ if __name__ == "__main__":
     gen_krylov()
     gen_diagnostics()
     gen_rank_fallback()
+    gen_printed_f()

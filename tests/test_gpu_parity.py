@@ -489,6 +489,18 @@ def test_rank_fallback_min_norm_vs_reference(hs, golden):
         _check(res, g, p, bitwise_basis=False, rtol=1e-8)
 
 
+def test_printed_f_variant_vs_reference(hs, golden):
+    """slslu_tikhonov(printed_f_columns=True): the comparison variant's penalty
+    columns S1 (A^T d_{k+1}) before the elimination (solvers.py:460-461,
+    488-490); pivots exact, the rest within the dense-problem tolerance."""
+    g = golden("printed_f")
+    A = hs.LinearOperator.from_matrix(g["M"])
+    cfg = hs.SolverConfig(maxiter=8, seed=6, lam=0.5)
+    _check(hs.slslu_tikhonov(A, g["b"], cfg, x_true=g["xt"], printed_f_columns=True), g, "pr_",
+           bitwise_basis=False, rtol=1e-9)
+    _check(hs.slslu_tikhonov(A, g["b"], cfg, x_true=g["xt"]), g, "df_", bitwise_basis=False, rtol=1e-9)
+
+
 def test_validation_errors(hs):
     A = hs.LinearOperator.from_matrix(np.eye(8) * 2.0 + 0.1)
     with pytest.raises(ValueError):
@@ -497,8 +509,8 @@ def test_validation_errors(hs):
         hs.scmrh(hs.LinearOperator.from_matrix(np.ones((3, 2))), np.ones(3), hs.SolverConfig(maxiter=2))
     with pytest.raises(ValueError):
         hs.slslu(A, np.ones(7), hs.SolverConfig(maxiter=2))
-    with pytest.raises(NotImplementedError):
-        hs.slslu_tikhonov(A, np.ones(8), hs.SolverConfig(maxiter=2, lam=0.1), printed_f_columns=True)
+    r = hs.slslu_tikhonov(A, np.ones(8), hs.SolverConfig(maxiter=2, lam=0.1), printed_f_columns=True)
+    assert len(r.trace.records) == 2 and np.all(np.isfinite(r.x))
     r = hs.scmrh(A, np.ones(8), hs.SolverConfig(maxiter=2, compute_diagnostics=True))
     assert all(rec.res_norm is not None and rec.kappa_basis is not None for rec in r.trace.records)
 

@@ -272,6 +272,17 @@ def test_rank_fallback_bitwise(golden):
     _check_result(res, g, "ll_")
 
 
+def test_printed_f_variant_bitwise(golden):
+    """slslu_tikhonov(printed_f_columns=True) (solvers.py:460-461, 488-490)."""
+    g = golden("printed_f")
+    A = ho.dense_operator(g["M"], sequential=False)
+    res = ho.hessenberg_solve(A, g["b"], square=False, maxiter=8, seed=6, lam=0.5, x_true=g["xt"], printed_f=True)
+    _check_result(res, g, "pr_")
+    res = ho.hessenberg_solve(A, g["b"], square=False, maxiter=8, seed=6, lam=0.5, x_true=g["xt"])
+    _check_result(res, g, "df_")
+    assert not np.allclose(g["pr_x"], g["df_x"])
+
+
 def _check_krylov(res, g, prefix):
     assert res.termination == str(g[prefix + "termination"])
     assert len(res.records) == len(g[prefix + "proj_obj"])
