@@ -15,6 +15,8 @@
  *   hs_sketch_create        SketchOperator / make_gaussian_sketch    sketch.py:29-53
  *   hs_sketch_apply         sketch_apply                             sketch.py:56-65
  *   hs_sketch_apply_many    entries @ Q (a block of vectors)         sketch.py:108
+ *   hs_stepper_*            init_square / step_square /              hessenberg.py:160-226,
+ *                           init_generalized / step_generalized      275-390
  *   hs_solve                _hessenberg_solve                        solvers.py:410-539
  *                           via scmrh / slslu / *_tikhonov           solvers.py:562-605
  *                           and cmrh / lslu (unsketched)             solvers.py:542-559
@@ -154,6 +156,32 @@ int hs_sketch_materialize(hs_sketch* sk, double* out);
 int hs_sketch_nnz(hs_sketch* sk, int64_t* nnz);
 int hs_sketch_export_csr(hs_sketch* sk, int64_t* indptr, int32_t* indices, double* data);
 int hs_sketch_destroy(hs_sketch* sk);
+
+/* step-level API (hessenberg.py:160-226 init_square / step_square,
+ * 275-390 init_generalized / step_generalized): the state stays on the device
+ * between calls.  `positions` (sampled pivoting only, else NULL): the host's
+ * rng.choice draws for this call's selection slots, [slot][pivot_sample], one
+ * slot (square) or two (rectangular: data side, then solution side).  When the
+ * starting residual (or A^T r0) is zero, *trivial is set to 1 (or 2) and no
+ * stepper is returned (the reference's TrivialSolution). */
+typedef struct hs_stepper hs_stepper;
+int hs_stepper_create(hs_ctx* ctx, hs_op* op, int32_t square, int32_t work_dtype, int32_t basis_dtype,
+                      int32_t capacity, const double* b, const double* x0, int32_t pivot_sample,
+                      const int64_t* positions, int32_t* trivial, hs_stepper** out);
+/* one step; HS_ERR_RUNTIME after a breakdown (hessenberg.py:201-202, 338-339) */
+int hs_stepper_step(hs_stepper* sp, int32_t keep_products, const int64_t* positions);
+int hs_stepper_info(const hs_stepper* sp, int32_t* k, int32_t* breakdown, int32_t* bd_side, int32_t* n_basis_sol,
+                    int32_t* n_basis_data, double* beta, double* alpha);
+/* H: (k+1) x k column-major; W: n_basis_data^2 column-major (rectangular) */
+int hs_stepper_hessenberg(hs_stepper* sp, double* H, double* W);
+/* pivot positions in selection order: t[n_basis_data], g[n_basis_sol] */
+int hs_stepper_pivots(hs_stepper* sp, int64_t* t, int64_t* g);
+/* basis column j (which: 0 = L, 1 = D) as float64 */
+int hs_stepper_basis(hs_stepper* sp, int32_t which, int32_t j, double* out);
+/* unreduced products of the last keep_products step: 0 = A l_k (m), 1 = A^T d_{k+1} (n) */
+int hs_stepper_product(hs_stepper* sp, int32_t which, double* out);
+int hs_stepper_r0(hs_stepper* sp, double* out);
+int hs_stepper_destroy(hs_stepper* sp);
 
 /* the solve: b[m], x0[n] or NULL, x_true[n] or NULL (host float64).
    Sketched: S2 required, S1 required iff cfg->lam > 0.  Unsketched: both NULL. */

@@ -9,7 +9,18 @@ The loop runs as hand-written sm_100a CUDA kernels behind the C ABI in
 no CPU fallback: without the library or a GPU every solve raises.
 """
 
-from .hessenberg import DeviceFactorization, PivotStrategy, TrivialSolution
+from .hessenberg import (
+    DeviceFactorization,
+    GeneralizedHessenbergState,
+    HessenbergState,
+    PivotStrategy,
+    TrivialSolution,
+    dump_factorization,
+    init_generalized,
+    init_square,
+    step_generalized,
+    step_square,
+)
 from .linops import (
     CsrOperator,
     DenseOperator,

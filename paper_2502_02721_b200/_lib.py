@@ -94,6 +94,16 @@ _SIGNATURES = [
     ("hs_result_projected", c_i32, [c_vp, c_vp, c_vp, c_vp]),
     ("hs_result_loop_ms", c_i32, [c_vp, P_dbl]),
     ("hs_result_destroy", c_i32, [c_vp]),
+    ("hs_stepper_create", c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, c_vp, c_i32, c_vp, P_i32,
+                                  ctypes.POINTER(c_vp)]),
+    ("hs_stepper_step", c_i32, [c_vp, c_i32, c_vp]),
+    ("hs_stepper_info", c_i32, [c_vp, P_i32, P_i32, P_i32, P_i32, P_i32, P_dbl, P_dbl]),
+    ("hs_stepper_hessenberg", c_i32, [c_vp, c_vp, c_vp]),
+    ("hs_stepper_pivots", c_i32, [c_vp, c_vp, c_vp]),
+    ("hs_stepper_basis", c_i32, [c_vp, c_i32, c_i32, c_vp]),
+    ("hs_stepper_product", c_i32, [c_vp, c_i32, c_vp]),
+    ("hs_stepper_r0", c_i32, [c_vp, c_vp]),
+    ("hs_stepper_destroy", c_i32, [c_vp]),
 ]
 
 EXPORTED = [name for name, _, _ in _SIGNATURES]

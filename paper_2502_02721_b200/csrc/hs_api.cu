@@ -1682,5 +1682,6 @@ int hs_ctx_synchronize(hs_ctx* ctx) { return guarded([&] { CK(cudaStreamSynchron
 
 #include "hs_krylov.inc"
 #include "hs_dist.inc"
+#include "hs_stepper.inc"
 
 #include "hs_abi.inc"
