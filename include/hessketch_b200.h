@@ -15,6 +15,7 @@
  *   hs_sketch_create        SketchOperator / make_gaussian_sketch    sketch.py:29-53
  *   hs_sketch_apply         sketch_apply                             sketch.py:56-65
  *   hs_sketch_apply_many    entries @ Q (a block of vectors)         sketch.py:108
+ *   hs_pivot_select         pivot_select                             hessenberg.py:93-115
  *   hs_stepper_*            init_square / step_square /              hessenberg.py:160-226,
  *                           init_generalized / step_generalized      275-390
  *   hs_solve                _hessenberg_solve                        solvers.py:410-539
@@ -164,6 +165,12 @@ int hs_sketch_destroy(hs_sketch* sk);
  * slot (square) or two (rectangular: data side, then solution side).  When the
  * starting residual (or A^T r0) is zero, *trivial is set to 1 (or 2) and no
  * stepper is returned (the reference's TrivialSolution). */
+/* pivot_select (hessenberg.py:93-115): largest |v| over the candidate rows
+ * cand[ncand] (the sampled subset already drawn by the host, or the full
+ * admissible set), ties -> smallest row index; all candidates zero ->
+ * (min(cand), 0.0).  v host float64 of length n. */
+int hs_pivot_select(hs_ctx* ctx, int64_t n, const double* v, int64_t ncand, const int64_t* cand, int64_t* idx,
+                    double* val);
 typedef struct hs_stepper hs_stepper;
 int hs_stepper_create(hs_ctx* ctx, hs_op* op, int32_t square, int32_t work_dtype, int32_t basis_dtype,
                       int32_t capacity, const double* b, const double* x0, int32_t pivot_sample,

@@ -18,6 +18,7 @@ from .hessenberg import (
     dump_factorization,
     init_generalized,
     init_square,
+    pivot_select,
     step_generalized,
     step_square,
 )

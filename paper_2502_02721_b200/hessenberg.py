@@ -30,6 +30,7 @@ __all__ = [
     "init_generalized",
     "step_generalized",
     "dump_factorization",
+    "pivot_select",
 ]
 
 
@@ -160,6 +161,29 @@ class DeviceFactorization:
         if self.square:
             raise AttributeError("square factorizations have no D")
         return np.column_stack(list(self.D_cols))
+
+
+def pivot_select(v, admissible, strategy, rng=None):
+    """hessenberg.py:93-115 on the device: ``(index, signed value)`` of the
+    largest |v| over the admissible rows, ties toward the smallest row index;
+    value 0.0 means every candidate was zero.  With a sampled strategy the
+    candidates are ``rng.choice(admissible, sample_size, replace=False)``
+    drawn here, as the reference draws them."""
+    from . import _lib
+
+    admissible = np.asarray(admissible, dtype=int)
+    if admissible.size == 0:
+        raise ValueError("admissible index set is empty")
+    if strategy.kind == "sampled" and strategy.sample_size < admissible.size:
+        if rng is None:
+            raise ValueError("sampled pivoting requires a random generator")
+        admissible = rng.choice(admissible, size=strategy.sample_size, replace=False)
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    cand = np.ascontiguousarray(admissible, dtype=np.int64)
+    idx, val = _lib.c_i64(), _lib.c_dbl()
+    _lib.check(_lib.load().hs_pivot_select(_lib.context().handle, v.size, _lib.ptr(v), cand.size, _lib.ptr(cand),
+                                           ctypes.byref(idx), ctypes.byref(val)))
+    return int(idx.value), float(val.value)
 
 
 # ---------------------------------------------------------------------------

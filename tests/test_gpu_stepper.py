@@ -136,3 +136,31 @@ def test_dump_factorization(hs, tmp_path):
     np.testing.assert_allclose(load_array(tmp_path / "f_H.mm"), st.H_matrix())
     np.testing.assert_allclose(load_array(tmp_path / "f_W.mm"), st.W_matrix())
     np.testing.assert_allclose(load_array(tmp_path / "f_pivots_g.mm").ravel(), st.g)
+
+
+def test_pivot_select_semantics(hs):
+    """pivot_select (hessenberg.py:93-115) on the device: signed value of the
+    largest |v|, ties toward the smallest row index whatever the listing order,
+    all-zero candidates -> value 0.0, sampling draws the reference's subset."""
+    full = hs.PivotStrategy.full()
+    v = np.array([3.0, -5.0, 2.0])
+    assert hs.pivot_select(v, [0, 1, 2], full) == (1, -5.0)
+    assert hs.pivot_select(v, [0, 2], full) == (0, 3.0)
+    v = np.array([2.0, -2.0, 2.0])
+    assert hs.pivot_select(v, [2, 1, 0], full) == (0, 2.0)
+    assert hs.pivot_select(v, [2, 1], full) == (1, -2.0)
+    assert hs.pivot_select(np.zeros(4), [1, 3], full)[1] == 0.0
+    with pytest.raises(ValueError):
+        hs.pivot_select(np.ones(3), [], full)
+    with pytest.raises(ValueError):
+        hs.pivot_select(np.ones(10), list(range(10)), hs.PivotStrategy.sampled(2))
+    rng = np.random.default_rng(4)
+    w = rng.standard_normal(50)
+    adm = np.arange(5, 50)
+    strat = hs.PivotStrategy.sampled(7, seed=1)
+    got = hs.pivot_select(w, adm, strat, np.random.default_rng(9))
+    sub = np.random.default_rng(9).choice(adm, size=7, replace=False)
+    i = int(sub[np.argmax(np.abs(w[sub]))])
+    assert got == (i, float(w[i]))
+    # sample size >= admissible size: the full set
+    assert hs.pivot_select(w, adm, hs.PivotStrategy.sampled(45), None) == hs.pivot_select(w, adm, full)
