@@ -16,6 +16,7 @@
  *   hs_sketch_apply         sketch_apply                             sketch.py:56-65
  *   hs_sketch_apply_many    entries @ Q (a block of vectors)         sketch.py:108
  *   hs_pivot_select         pivot_select                             hessenberg.py:93-115
+ *   hs_projected_ls         dense_qr_ls / stacked_tikhonov_ls        linops.py:168-229
  *   hs_stepper_*            init_square / step_square /              hessenberg.py:160-226,
  *                           init_generalized / step_generalized      275-390
  *   hs_solve                _hessenberg_solve                        solvers.py:410-539
@@ -171,6 +172,12 @@ int hs_sketch_destroy(hs_sketch* sk);
  * (min(cand), 0.0).  v host float64 of length n. */
 int hs_pivot_select(hs_ctx* ctx, int64_t n, const double* v, int64_t ncand, const int64_t* cand, int64_t* idx,
                     double* val);
+/* dense_qr_ls (linops.py:168-207): min |M y - rhs| for an l x k column-major
+ * M (l >= k) with the loop's incremental QR; y = the minimum-norm solution
+ * when the 1e-14 rank gate fires, *rank = k - dependent columns (the caller
+ * raises RankDeficiencyError when *rank < k).  stacked_tikhonov_ls
+ * (linops.py:210-229) is this on [M; lam N] with rhs [rhs; 0]. */
+int hs_projected_ls(hs_ctx* ctx, int64_t l, int32_t k, const double* M, const double* rhs, double* y, int32_t* rank);
 typedef struct hs_stepper hs_stepper;
 int hs_stepper_create(hs_ctx* ctx, hs_op* op, int32_t square, int32_t work_dtype, int32_t basis_dtype,
                       int32_t capacity, const double* b, const double* x0, int32_t pivot_sample,

@@ -29,7 +29,11 @@ from .linops import (
     LinearOperator,
     OpCounters,
     PsfOperator,
+    RANK_TOL,
+    RankDeficiencyError,
     TomographyOperator,
+    dense_qr_ls,
+    stacked_tikhonov_ls,
     to_device_operator,
 )
 from .sketch import (

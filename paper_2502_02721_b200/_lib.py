@@ -105,6 +105,7 @@ _SIGNATURES = [
     ("hs_stepper_r0", c_i32, [c_vp, c_vp]),
     ("hs_stepper_destroy", c_i32, [c_vp]),
     ("hs_pivot_select", c_i32, [c_vp, c_i64, c_vp, c_i64, c_vp, P_i64, P_dbl]),
+    ("hs_projected_ls", c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, P_i32]),
 ]
 
 EXPORTED = [name for name, _, _ in _SIGNATURES]

@@ -369,3 +369,60 @@ def load_operator(path):
     with open(path, "rb") as fh:
         M = scipy.io.mmread(fh)
     return LinearOperator.from_matrix(M)
+
+
+# ---------------------------------------------------------------------------
+# projected least squares (linops.py:34-50, 168-229) on the device
+
+
+RANK_TOL = 1e-14
+
+
+class RankDeficiencyError(np.linalg.LinAlgError):
+    """linops.py:39-50: raised with the detected numerical rank."""
+
+    def __init__(self, message, rank):
+        super().__init__(message)
+        self.rank = rank
+
+
+def dense_qr_ls(M, rhs):
+    """linops.py:168-207 on the device: min_y |M y - rhs| for l >= k, by the
+    loop's incremental CGS2 QR (hs_qr.cuh).  Raises RankDeficiencyError when a
+    column fails the RANK_TOL gate (the solvers then use the minimum-norm
+    solution, which the device forms from the same factorisation)."""
+    M = np.asarray(M, dtype=float)
+    rhs = np.asarray(rhs, dtype=float)
+    if M.ndim != 2:
+        raise ValueError("M must be 2-D")
+    l, k = M.shape
+    if l < k:
+        raise ValueError(f"need at least as many rows as columns, got {M.shape}")
+    if rhs.shape != (l,):
+        raise ValueError(f"rhs must have length {l}, got shape {rhs.shape}")
+    if k == 0:
+        return np.empty(0)
+    Mc = np.asfortranarray(M)
+    rhs = np.ascontiguousarray(rhs)
+    y = np.empty(k)
+    rank = _lib.c_i32()
+    _lib.check(_lib.load().hs_projected_ls(_lib.context().handle, l, k, ctypes.c_void_p(Mc.ctypes.data), _lib.ptr(rhs),
+                                           _lib.ptr(y), ctypes.byref(rank)))
+    if rank.value < k:
+        raise RankDeficiencyError(f"matrix is numerically rank deficient (rank {rank.value} of {k})", rank.value)
+    return y
+
+
+def stacked_tikhonov_ls(M, N, rhs, lam):
+    """linops.py:210-229: min |M y - rhs|^2 + lam^2 |N y|^2 as the stacked
+    system [M; lam N] y ~ [rhs; 0]; lam == 0 takes exactly dense_qr_ls."""
+    if lam < 0:
+        raise ValueError("lam must be nonnegative")
+    if lam == 0.0:
+        return dense_qr_ls(M, rhs)
+    M = np.asarray(M, dtype=float)
+    N = np.asarray(N, dtype=float)
+    rhs = np.asarray(rhs, dtype=float)
+    if N.shape[1] != M.shape[1]:
+        raise ValueError("M and N must have the same number of columns")
+    return dense_qr_ls(np.vstack([M, lam * N]), np.concatenate([rhs, np.zeros(N.shape[0])]))
