@@ -526,7 +526,12 @@ struct hs_op {
       } else if (M.d16) {
         int gshift = -1;
         if (img_grid > 0 && (img_grid & (img_grid - 1)) == 0) gshift = __builtin_ctz((unsigned)img_grid);
-        auto kern = (gshift >= 0 || !tflag) ? sell_spmv_d16_kernel<V, Tin, T, true> : sell_spmv_d16_kernel<V, Tin, T, false>;
+        // few slices (< 2 per resident warp): the walk is latency-bound, use the deeper pipeline
+        const bool deep = env_flag("HS_D16_DEEP") ||
+                          (M.nslices < 2LL * ctx->num_sms * 48 && !env_flag("HS_D16_SHALLOW"));
+        const bool p2 = gshift >= 0 || !tflag;
+        auto kern = deep ? (p2 ? sell_spmv_d16_kernel<V, Tin, T, true, true> : sell_spmv_d16_kernel<V, Tin, T, false, true>)
+                         : (p2 ? sell_spmv_d16_kernel<V, Tin, T, true> : sell_spmv_d16_kernel<V, Tin, T, false>);
         kern<<<grid, 256, 0, s>>>(M.rows, M.nslices, M.sptr.as<long long>(), M.rlen.as<int>(), M.rbase.as<int>(),
                                   M.dcol.as<short>(), M.val.as<V>(), xi, tflag ? xT.as<Tin>() : nullptr,
                                   tflag ? sflag.as<unsigned char>() : nullptr, img_grid, gshift >= 0 ? gshift : 0,

@@ -593,8 +593,67 @@ __device__ __forceinline__ T d16_row(const short* __restrict__ dp, const V* __re
   return acc;
 }
 
-template <class V, class Tin, class T, bool POW2>
-__global__ void __launch_bounds__(256, (sizeof(T) == 4 && sizeof(V) == 4) ? 6 : 3)
+// Deeper pipeline for operators with few slices (fewer than ~2 per resident
+// warp, e.g. config 3): there the kernel is bound by each lane's serial walk
+// (one dependent gather round trip per chunk), not by the stream, so chunk
+// q+1's gathers are issued before chunk q's adds and the (delta, value)
+// stream runs two chunks ahead.  Same products, same order of adds.
+template <int GM, class V, class Tin, class T>
+__device__ __forceinline__ void d16_gather4(int& c, const int2 d, const Tin* __restrict__ x, int m, int sh, int grid,
+                                            T (&g)[4]) {
+  const int c0 = c + (int)(short)(d.x & 0xffff);
+  const int c1 = c0 + (d.x >> 16);
+  const int c2 = c1 + (int)(short)(d.y & 0xffff);
+  const int c3 = c2 + (d.y >> 16);
+  g[0] = gather_x<T>(x, gpos<GM>(c0, m, sh, grid));
+  g[1] = gather_x<T>(x, gpos<GM>(c1, m, sh, grid));
+  g[2] = gather_x<T>(x, gpos<GM>(c2, m, sh, grid));
+  g[3] = gather_x<T>(x, gpos<GM>(c3, m, sh, grid));
+  c = c3;
+}
+
+template <int GM, class V, class Tin, class T>
+__device__ __forceinline__ T d16_row_deep(const short* __restrict__ dp, const V* __restrict__ vp, int c, int len,
+                                          const Tin* __restrict__ x, int m, int sh, int grid) {
+  T acc = T(0);
+  const int nq = (len + 3) >> 2;
+  if (nq == 0) return acc;
+  Chunk4<V> v = Chunk4<V>::load(vp);
+  T g[4];
+  d16_gather4<GM, V, Tin, T>(c, __ldcs(reinterpret_cast<const int2*>(dp)), x, m, sh, grid, g);
+  int2 dn = make_int2(0, 0);
+  Chunk4<V> vn = v;
+  if (nq > 1) {
+    dn = __ldcs(reinterpret_cast<const int2*>(dp + 128));
+    vn = Chunk4<V>::load(vp + 128);
+  }
+  for (int q = 0; q < nq; ++q) {
+    T gn[4] = {T(0), T(0), T(0), T(0)};
+    int2 dnn = dn;
+    Chunk4<V> vnn = vn;
+    if (q + 1 < nq) {
+      d16_gather4<GM, V, Tin, T>(c, dn, x, m, sh, grid, gn);  // padding deltas are 0: valid addresses
+      if (q + 2 < nq) {
+        dnn = __ldcs(reinterpret_cast<const int2*>(dp + (long long)(q + 2) * 128));
+        vnn = Chunk4<V>::load(vp + (long long)(q + 2) * 128);
+      }
+    }
+    const int nv = min(4, len - 4 * q);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (i < nv) acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[i]), g[i]));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) g[i] = gn[i];
+    v = vn;
+    vn = vnn;
+    dn = dnn;
+  }
+  return acc;
+}
+
+template <class V, class Tin, class T, bool POW2, bool DEEP = false>
+__global__ void __launch_bounds__(256, DEEP ? ((sizeof(T) == 4 && sizeof(V) == 4) ? 4 : 2)
+                                            : ((sizeof(T) == 4 && sizeof(V) == 4) ? 6 : 3))
 sell_spmv_d16_kernel(long long rows, long long nslices, const long long* __restrict__ sptr,
                      const int* __restrict__ rlen, const int* __restrict__ rbase, const short* __restrict__ dcol,
                      const V* __restrict__ val, const Tin* __restrict__ xrow, const Tin* __restrict__ xT,
@@ -618,9 +677,15 @@ sell_spmv_d16_kernel(long long rows, long long nslices, const long long* __restr
     const short* dp = dcol + base + lane * 4;
     const V* vp = val + base + lane * 4;
     T acc;
-    if (!tr) acc = d16_row<0, V, Tin, T>(dp, vp, c, len, xrow, 0, 0, grid);
-    else if (POW2) acc = d16_row<1, V, Tin, T>(dp, vp, c, len, xT, grid - 1, gshift, grid);
-    else acc = d16_row<2, V, Tin, T>(dp, vp, c, len, xT, 0, 0, grid);
+    if (DEEP) {
+      if (!tr) acc = d16_row_deep<0, V, Tin, T>(dp, vp, c, len, xrow, 0, 0, grid);
+      else if (POW2) acc = d16_row_deep<1, V, Tin, T>(dp, vp, c, len, xT, grid - 1, gshift, grid);
+      else acc = d16_row_deep<2, V, Tin, T>(dp, vp, c, len, xT, 0, 0, grid);
+    } else {
+      if (!tr) acc = d16_row<0, V, Tin, T>(dp, vp, c, len, xrow, 0, 0, grid);
+      else if (POW2) acc = d16_row<1, V, Tin, T>(dp, vp, c, len, xT, grid - 1, gshift, grid);
+      else acc = d16_row<2, V, Tin, T>(dp, vp, c, len, xT, 0, 0, grid);
+    }
     if (row >= 0 && row < rows) y[row] = acc;
   }
   // the last warp out resets the scheduler for the next launch
