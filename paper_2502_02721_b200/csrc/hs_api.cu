@@ -595,7 +595,11 @@ struct hs_op {
   void psf_launch(const Tin* xi, int rows, int out_row0, int out_rows, T* yo, bool transpose) const {
     cudaStream_t s = ctx->stream;
     Prof p(ctx, "psf_stencil", (double)out_rows * W * (sizeof(Tin) + sizeof(T)));
-    if ((kw == 15 || kw == 31) && !env_flag("HS_PSF_SIMPLE")) {
+    // register-blocked tiles (128 x 16 outputs) when they fill the GPU; small
+    // images (config 2: 256^2 -> 32 tiles) keep the 32 x 8 tiles of the simple kernel
+    const long long rb_tiles = (long long)((W + 127) / 128) * ((out_rows + 15) / 16);
+    if ((kw == 15 || kw == 31) && !env_flag("HS_PSF_SIMPLE") &&
+        (rb_tiles >= 2LL * ctx->num_sms || env_flag("HS_PSF_RB"))) {
       auto launch = [&](auto kwc) {
         constexpr int KWc = decltype(kwc)::value;
         using G = PsfRb<T, KWc>;

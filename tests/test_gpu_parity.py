@@ -90,10 +90,13 @@ def test_dense_operator_bitwise_sequential(hs):
     np.testing.assert_array_equal(op32.matvec(x.astype(np.float32), np.float32), ho.sequential_rows(M32, x.astype(np.float32)))
 
 
+@pytest.mark.parametrize("kernel", ["auto", "rb"])
 @pytest.mark.parametrize("dt", [np.float64, np.float32])
 @pytest.mark.parametrize("shape,ks", [((16, 16), (5, 5)), ((33, 70), (3, 7)), ((64, 64), (15, 15)),
                                       ((150, 270), (31, 31)), ((37, 129), (9, 15)), ((70, 300), (31, 15))])
-def test_psf_stencil_bitwise(hs, dt, shape, ks):
+def test_psf_stencil_bitwise(hs, monkeypatch, dt, shape, ks, kernel):
+    if kernel == "rb":  # force the register-blocked kernel on these small images
+        monkeypatch.setenv("HS_PSF_RB", "1")
     rng = np.random.default_rng(5)
     K = rng.random(ks)
     K /= K.sum()
