@@ -146,7 +146,7 @@ def run_ours(args, ws, rank, local):
 
     import paper_2502_02721_b200 as hs
     from paper_2502_02721_b200 import _lib
-    from paper_2502_02721_b200.problems import make_workload
+    from paper_2502_02721_b200.problems import CONFIGS, make_workload
 
     os.environ["HS_DEVICE"] = str(local)
     _lib.load()
@@ -220,7 +220,7 @@ def run_ours(args, ws, rank, local):
         "dtype": "f32",
         "data": "synthetic (seeded random-ellipse phantom, 1% noise; device-built exact-chord operator)",
         "config": {
-            "workload": f"cfg{args.config}: " + w.name,
+            "workload": f"cfg{args.config}: " + CONFIGS[args.config],
             "grid": w.meta.get("grid"), "angles": w.meta.get("angles"), "bins": w.meta.get("bins"),
             "nnz": inf.get("nnz"), "maxiter": K, "sketch": "sparse-sign ell=%d zeta=8" % w.cfg.sketch_rows,
             "step": "one full sLSLU solve (maxiter iterations)",
