@@ -530,8 +530,19 @@ struct hs_op {
         const bool deep = env_flag("HS_D16_DEEP") ||
                           (M.nslices < 2LL * ctx->num_sms * 48 && !env_flag("HS_D16_SHALLOW"));
         const bool p2 = gshift >= 0 || !tflag;
-        auto kern = deep ? (p2 ? sell_spmv_d16_kernel<V, Tin, T, true, true> : sell_spmv_d16_kernel<V, Tin, T, false, true>)
-                         : (p2 ? sell_spmv_d16_kernel<V, Tin, T, true> : sell_spmv_d16_kernel<V, Tin, T, false>);
+        // pipeline depth in chunks per gather step (HS_D16_PIPE overrides for A/B runs)
+        // (fewer slices than ~32 per SM, e.g. config 3's A: 4,078 slices of 460-entry rays: depth 2,
+        // 0.157 -> 0.107 ms; its A^T, 8,192 shorter slices, stays at depth 1: 0.091 vs 0.106 ms)
+        int depth = deep ? (M.nslices < 32LL * ctx->num_sms ? 2 : 1) : 0;
+        if (const char* e = getenv("HS_D16_PIPE")) depth = atoi(e);
+        auto pick = [&](auto p2c) {
+          constexpr bool P2 = decltype(p2c)::value;
+          return depth >= 4 ? sell_spmv_d16_kernel<V, Tin, T, P2, 4>
+               : depth == 2 ? sell_spmv_d16_kernel<V, Tin, T, P2, 2>
+               : depth == 1 ? sell_spmv_d16_kernel<V, Tin, T, P2, 1>
+                            : sell_spmv_d16_kernel<V, Tin, T, P2, 0>;
+        };
+        auto kern = p2 ? pick(std::true_type{}) : pick(std::false_type{});
         kern<<<grid, 256, 0, s>>>(M.rows, M.nslices, M.sptr.as<long long>(), M.rlen.as<int>(), M.rbase.as<int>(),
                                   M.dcol.as<short>(), M.val.as<V>(), xi, tflag ? xT.as<Tin>() : nullptr,
                                   tflag ? sflag.as<unsigned char>() : nullptr, img_grid, gshift >= 0 ? gshift : 0,

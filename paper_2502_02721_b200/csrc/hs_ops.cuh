@@ -651,9 +651,90 @@ __device__ __forceinline__ T d16_row_deep(const short* __restrict__ dp, const V*
   return acc;
 }
 
-template <class V, class Tin, class T, bool POW2, bool DEEP = false>
-__global__ void __launch_bounds__(256, DEEP ? ((sizeof(T) == 4 && sizeof(V) == 4) ? 4 : 2)
-                                            : ((sizeof(T) == 4 && sizeof(V) == 4) ? 6 : 3))
+// Group pipeline of depth U (U >= 2) for operators with far fewer slices than
+// warp slots (config 3): the kernel time is the longest slice's walk, one
+// gather round trip per step, so each step covers U chunks: the gathers of
+// group g+1 (4U loads) are in flight while group g is added, and the stream
+// runs two groups ahead.  Registers grow ~22U per thread, which costs nothing
+// when resident warps outnumber the slices.  Same products, same add order.
+template <int GM, int U, class V, class Tin, class T>
+__device__ __forceinline__ void d16_group_gather(int& c, const int2 (&d)[U], int q0, int nq,
+                                                 const Tin* __restrict__ x, int m, int sh, int grid, T (&g)[U][4]) {
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    if (q0 + u < nq) {
+      const int c0 = c + (int)(short)(d[u].x & 0xffff);
+      const int c1 = c0 + (d[u].x >> 16);
+      const int c2 = c1 + (int)(short)(d[u].y & 0xffff);
+      const int c3 = c2 + (d[u].y >> 16);
+      g[u][0] = gather_x<T>(x, gpos<GM>(c0, m, sh, grid));
+      g[u][1] = gather_x<T>(x, gpos<GM>(c1, m, sh, grid));
+      g[u][2] = gather_x<T>(x, gpos<GM>(c2, m, sh, grid));
+      g[u][3] = gather_x<T>(x, gpos<GM>(c3, m, sh, grid));
+      c = c3;
+    }
+  }
+}
+
+template <int U>
+__device__ __forceinline__ void d16_group_dload(const short* __restrict__ dp, int q0, int nq, int2 (&d)[U]) {
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (q0 + u < nq) d[u] = __ldcs(reinterpret_cast<const int2*>(dp + (long long)(q0 + u) * 128));
+}
+
+template <int U, class V>
+__device__ __forceinline__ void d16_group_vload(const V* __restrict__ vp, int q0, int nq, Chunk4<V> (&v)[U]) {
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (q0 + u < nq) v[u] = Chunk4<V>::load(vp + (long long)(q0 + u) * 128);
+}
+
+// deltas run two groups ahead, values and gathers one group ahead
+template <int GM, int U, class V, class Tin, class T>
+__device__ __forceinline__ T d16_row_pipe(const short* __restrict__ dp, const V* __restrict__ vp, int c, int len,
+                                          const Tin* __restrict__ x, int m, int sh, int grid) {
+  T acc = T(0);
+  const int nq = (len + 3) >> 2;
+  if (nq == 0) return acc;
+  const int ng = (nq + U - 1) / U;
+  int2 dA[U], dB[U];
+  Chunk4<V> vC[U];
+  T gC[U][4];
+  d16_group_dload<U>(dp, 0, nq, dA);
+  d16_group_vload<U, V>(vp, 0, nq, vC);
+  d16_group_gather<GM, U, V, Tin, T>(c, dA, 0, nq, x, m, sh, grid, gC);
+  if (ng > 1) d16_group_dload<U>(dp, U, nq, dA);
+#pragma unroll 1
+  for (int gi = 0; gi < ng; ++gi) {
+    if (gi + 2 < ng) d16_group_dload<U>(dp, (gi + 2) * U, nq, dB);
+    T gN[U][4];
+    Chunk4<V> vN[U];
+    if (gi + 1 < ng) {
+      d16_group_vload<U, V>(vp, (gi + 1) * U, nq, vN);
+      d16_group_gather<GM, U, V, Tin, T>(c, dA, (gi + 1) * U, nq, x, m, sh, grid, gN);
+    }
+    const int e0 = gi * U * 4;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (e0 + u * 4 + i < len) acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(vC[u].v[i]), gC[u][i]));
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      vC[u] = vN[u];
+      dA[u] = dB[u];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) gC[u][i] = gN[u][i];
+    }
+  }
+  return acc;
+}
+
+template <class V, class Tin, class T, bool POW2, int DEPTH = 0>
+__global__ void __launch_bounds__(256, DEPTH == 0 ? ((sizeof(T) == 4 && sizeof(V) == 4) ? 6 : 3)
+                                       : DEPTH == 1 ? ((sizeof(T) == 4 && sizeof(V) == 4) ? 4 : 2)
+                                       : DEPTH == 2 ? 2 : 1)
 sell_spmv_d16_kernel(long long rows, long long nslices, const long long* __restrict__ sptr,
                      const int* __restrict__ rlen, const int* __restrict__ rbase, const short* __restrict__ dcol,
                      const V* __restrict__ val, const Tin* __restrict__ xrow, const Tin* __restrict__ xT,
@@ -677,7 +758,11 @@ sell_spmv_d16_kernel(long long rows, long long nslices, const long long* __restr
     const short* dp = dcol + base + lane * 4;
     const V* vp = val + base + lane * 4;
     T acc;
-    if (DEEP) {
+    if constexpr (DEPTH >= 2) {
+      if (!tr) acc = d16_row_pipe<0, DEPTH, V, Tin, T>(dp, vp, c, len, xrow, 0, 0, grid);
+      else if (POW2) acc = d16_row_pipe<1, DEPTH, V, Tin, T>(dp, vp, c, len, xT, grid - 1, gshift, grid);
+      else acc = d16_row_pipe<2, DEPTH, V, Tin, T>(dp, vp, c, len, xT, 0, 0, grid);
+    } else if constexpr (DEPTH == 1) {
       if (!tr) acc = d16_row_deep<0, V, Tin, T>(dp, vp, c, len, xrow, 0, 0, grid);
       else if (POW2) acc = d16_row_deep<1, V, Tin, T>(dp, vp, c, len, xT, grid - 1, gshift, grid);
       else acc = d16_row_deep<2, V, Tin, T>(dp, vp, c, len, xT, 0, 0, grid);
