@@ -246,6 +246,9 @@ def run_ours(args, ws, rank, local):
         "gpu_launches": int(launches),
         "clocks": clocks,
         "kernels": kernels,
+        "kernels_note": ("CUDA-event spans per kernel name; aux-stream kernels (sketch_*, qr_step) are timed on "
+                         "the aux stream, so their span includes waiting for SM residency behind the main-stream "
+                         "SpMV they overlap"),
         "setup_s": round(setup_s, 2),
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

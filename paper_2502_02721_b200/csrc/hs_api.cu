@@ -992,7 +992,7 @@ struct Solver {
         Gb((size_t)ell * (K + 2) * sizeof(double)), sr0(ell * sizeof(double));
     DBuf Qb((size_t)ldq * K * sizeof(double)), Rinv((size_t)K * K * sizeof(double)), Rdiag(K * sizeof(double)),
         yb(K * sizeof(double)), Yh((size_t)K * K * sizeof(double));
-    const int NB = std::max(1, std::min(64, (Ls + 47) / 48));
+    const int NB = qr_blocks(Ls);
     DBuf part((size_t)4 * NB * (K + 2) * sizeof(double));
     DBuf sresb(K * sizeof(double)), projb(K * sizeof(double)), rfb(K * sizeof(int)), rel2((K + 1) * sizeof(double));
     const int CAND_CAP = (int)std::min<long long>(1LL << 20, std::max<long long>(4096, (std::max(ldm, ldn) / VEC + 255) / 256));
@@ -1233,19 +1233,22 @@ struct Solver {
     DBuf Nnull((size_t)K * K * sizeof(double)), ndrop(sizeof(int));
     qa.Nnull = Nnull.as<double>(); qa.ndrop = ndrop.as<int>();
     const size_t qr_smem = qr_smem_bytes(Ls, NB, K);
-    if (qr_smem > 48 * 1024)
-      CK(cudaFuncSetAttribute(qr_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qr_smem));
+    CK(prepare_qr_step(qr_smem));
     const bool rec_x = cfg.record_x && xt_h;
     const size_t elim_smem_base = 16;
     auto elim = [&](T* vec, long long len, long long ldv, const B* basis, int k, int side, int iter, int kx,
                     const double* yx, double* relerr_slot, T* vout) {
-      const long long nvec = (len + VEC - 1) / VEC;
+      // short vectors (configs 1-3): one element per thread, so the pass spreads
+      // over every SM and each thread keeps 16 basis loads in flight
+      const bool v1 = (len + VEC - 1) / VEC < 2LL * ctx->num_sms * 256 && !env_flag("HS_ELIM_VEC");
+      const long long nvec = v1 ? len : (len + VEC - 1) / VEC;
       const int g = grid_for(nvec, 256, CAND_CAP);
       const size_t smem = ((k * sizeof(T) + 15) / 16) * 16 + (size_t)kx * sizeof(double) + elim_smem_base;
       const double bytes = (double)std::max(k, kx) * len * sizeof(B) + 2.0 * len * sizeof(T) +
                            (kx ? (double)len * 8 : 0.0);
       Prof p(ctx, side == 0 && !square ? "elim_D" : "elim_L", bytes);
-      auto kern = kx ? elim_pass_kernel<T, B, VEC, true> : elim_pass_kernel<T, B, VEC, false>;
+      auto kern = v1 ? (kx ? elim_pass_kernel<T, B, 1, true> : elim_pass_kernel<T, B, 1, false>)
+                     : (kx ? elim_pass_kernel<T, B, VEC, true> : elim_pass_kernel<T, B, VEC, false>);
       if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       (void)ldv;
       kern<<<g, 256, smem, s>>>(
@@ -1309,8 +1312,7 @@ struct Solver {
         qa.fcol = lamon ? Fb.as<double>() + (long long)(kk - 1) * ell : nullptr;
         Prof p(ctx, "qr_step", 0.0, s2);
         int k1 = kk, it = kk;
-        void* args[] = {&qa, &k1, &it};
-        CK(cudaLaunchCooperativeKernel((void*)qr_step_kernel, dim3(NB), dim3(256), args, qr_smem, s2));
+        CK(launch_qr_step(qa, k1, it, NB, qr_smem, s2));
         ++g_launches;
       }
       CK(cudaEventRecord(ev_qrb[bidx], s2));
@@ -1351,8 +1353,20 @@ struct Solver {
       }
       op->apply(Lcol(k - 1), bdt, ucur, wdt, false);
       if (diag_eps) qW.append(u.as<T>());  // the unreduced A l_k (solvers.py:480-481)
+      // rectangular: the sketch of u (and the projected solve after it) starts
+      // once the data side is normalised, so the aux stream overlaps the long
+      // A^T apply instead of competing with the D elimination pass for the SMs
+      const bool defer_sk = ovl && SB == 1 && !square && !env_flag("HS_SK_EARLY");
+      auto sketch_u = [&] {
+        CK(cudaEventRecord(ev_u, s));
+        CK(cudaStreamWaitEvent(s2, ev_u, 0));
+        S2->apply(u.p, wdt, Zb.as<double>() + (long long)(k - 1) * ell, s2);
+        CK(cudaEventRecord(ev_sk, s2));
+      };
       if (SB > 1) {
         // sketched in batches (flush_batch)
+      } else if (defer_sk) {
+        // launched after normalize (below)
       } else if (ovl) {
         CK(cudaEventRecord(ev_u, s));
         CK(cudaStreamWaitEvent(s2, ev_u, 0));
@@ -1378,6 +1392,7 @@ struct Solver {
                              cudaMemcpyDeviceToDevice, s));
         normalize_kernel<T, B><<<grid_for(ldm, 256, NORM_G), 256, 0, s>>>(m, ldm, uel, pv.as<T>(), Dcol(k), st, 0, k);
         CKL();
+        if (defer_sk) sketch_u();
         if (sb) S2->apply(Dcol(k), bdt, Gb.as<double>() + (long long)k * ell);
         op->apply(Dcol(k), bdt, q.p, wdt, true);
         // printed variant: F column k = S1 q before the elimination (solvers.py:488-490)
@@ -1420,8 +1435,7 @@ struct Solver {
       if (SB == 1) {
         Prof p(ctx, "qr_step", 0.0, s2);
         int kk = k, it = k;
-        void* args[] = {&qa, &kk, &it};
-        CK(cudaLaunchCooperativeKernel((void*)qr_step_kernel, dim3(NB), dim3(256), args, qr_smem, s2));
+        CK(launch_qr_step(qa, kk, it, NB, qr_smem, s2));
         ++g_launches;
       }
       if (ovl && SB == 1) CK(cudaEventRecord(ev_qr, s2));

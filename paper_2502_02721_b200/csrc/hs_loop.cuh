@@ -126,6 +126,9 @@ fsub_block_kernel(const T* __restrict__ u, const long long* __restrict__ pos, lo
 // --------------------------------------------------------------------------
 // vector load helpers for the basis pass
 template <class B, int VEC> struct VecLoad;
+template <class B> struct VecLoad<B, 1> {
+  static __device__ __forceinline__ void ld(const B* p, B (&o)[1]) { o[0] = __ldg(p); }
+};
 template <> struct VecLoad<float, 4> {
   static __device__ __forceinline__ void ld(const float* p, float (&o)[4]) {
     float4 t = __ldg(reinterpret_cast<const float4*>(p));
@@ -193,7 +196,7 @@ elim_pass_kernel(long long n, long long idx_offset, const B* __restrict__ basis,
     }
     const B* bp = basis + e0;
     // kx <= k always (x of the previous iteration uses the first k-1 columns)
-    constexpr int UNR = XF ? 4 : 8;
+    constexpr int UNR = VEC == 1 ? 16 : (XF ? 4 : 8);
 #pragma unroll UNR
     for (int j = 0; j < k; ++j) {
       B b[VEC];

@@ -45,7 +45,7 @@ struct QrArgs {
   const double* F;      // ell x (kmax+1) (ld = ell) or null
   const double* sr0;    // ell
   double* Q;            // ldq x kmax
-  double* Rinv;         // kmax x kmax, column-major
+  double* Rinv;         // kmax x kmax, row-major (Rinv[i * kmax + l] = (R^{-1})_{il})
   double* Rdiag;        // kmax
   double* y;            // kmax (current solution)
   double* Yhist;        // kmax x kmax: y^{(k)} in column k-1
@@ -58,9 +58,12 @@ struct QrArgs {
   LoopState* st;
 };
 
+// CTAs of one projected-solve step: ~48 rows each, at most 64
+inline int qr_blocks(int Ls) { return Ls < 48 ? 1 : (Ls + 47) / 48 < 64 ? (Ls + 47) / 48 : 64; }
+
 // dynamic shared memory of qr_step_kernel
 inline size_t qr_smem_bytes(int Ls, int NB, int kmax) {
-  return ((size_t)((Ls + NB - 1) / NB) + 4 * (size_t)kmax) * sizeof(double);
+  return (2 * (size_t)((Ls + NB - 1) / NB) + 4 * (size_t)kmax + 256) * sizeof(double);
 }
 
 // out[i] = sum_{r < nr} Q[i*ldq + r] * v[r] for i < j: one warp per column,
@@ -101,6 +104,27 @@ __device__ __forceinline__ double block_max(double v, double* scratch) {
   return r;
 }
 
+// out[r] = sum_{i < ncol} elem(i, r) * coef[i] for r < nr (256 threads): four
+// column groups of 64 threads (i = g, g+4, ...; each warp reads 32
+// consecutive rows of one column), partials combined as (p0+p1)+(p2+p3).
+// A fixed order; the dependent fma chain is ncol/4 long instead of ncol.
+template <class F>
+__device__ __forceinline__ void split_rows(int nr, int ncol, const double* coef, F elem, double* red, double* out) {
+  const int t = threadIdx.x, g = t >> 6, rr = t & 63;
+  for (int rb = 0; rb < nr; rb += 64) {
+    const int r = rb + rr;
+    double s = 0.0;
+    if (r < nr) {
+#pragma unroll 8
+      for (int i = g; i < ncol; i += 4) s = fma(elem(i, r), coef[i], s);
+    }
+    red[g * 64 + rr] = s;
+    __syncthreads();
+    if (t < 64 && rb + t < nr) out[rb + t] = (red[t] + red[64 + t]) + (red[128 + t] + red[192 + t]);
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(256) qr_step_kernel(QrArgs a, int k, int iter) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
@@ -122,6 +146,8 @@ __global__ void __launch_bounds__(256) qr_step_kernel(QrArgs a, int k, int iter)
   double* c1s = cv + a.kmax;  // kmax (saved c1)
   double* wv = c1s + a.kmax;  // kmax (R^{-1} r of the new column / null vector)
   double* gv = wv + a.kmax;   // kmax (projection coefficients)
+  double* red = gv + a.kmax;  // 256 (split_rows partials)
+  double* mv = red + 256;     // RS (split_rows results)
   __shared__ double scratch[32];
 
   // phase 1: load the new stacked column, partial Q^T a
@@ -142,12 +168,10 @@ __global__ void __launch_bounds__(256) qr_step_kernel(QrArgs a, int k, int iter)
     c1s[i] = s;
   }
   __syncthreads();
-  for (int r = tid; r < nr; r += BT) {
-    double s = 0.0;
-    #pragma unroll 8
-    for (int i = 0; i < j; ++i) s = fma(a.Q[(long long)i * a.ldq + r0 + r], cv[i], s);
-    av[r] -= s;
-  }
+  const double* Qb = a.Q + r0;
+  const long long ldq = a.ldq;
+  split_rows(nr, j, cv, [&](int i, int r) { return Qb[(long long)i * ldq + r]; }, red, mv);
+  for (int r = tid; r < nr; r += BT) av[r] -= mv[r];
   __syncthreads();
   block_dots(a.Q + r0, a.ldq, j, av, nr, P2 + (long long)b * pld);
   grid.sync();
@@ -160,12 +184,10 @@ __global__ void __launch_bounds__(256) qr_step_kernel(QrArgs a, int k, int iter)
     cv[i] = s;
   }
   __syncthreads();
+  split_rows(nr, j, cv, [&](int i, int r) { return Qb[(long long)i * ldq + r]; }, red, mv);
   double nn = 0.0, ar = 0.0;
   for (int r = tid; r < nr; r += BT) {
-    double s = 0.0;
-    #pragma unroll 8
-    for (int i = 0; i < j; ++i) s = fma(a.Q[(long long)i * a.ldq + r0 + r], cv[i], s);
-    const double v = av[r] - s;
+    const double v = av[r] - mv[r];
     av[r] = v;
     nn = fma(v, v, nn);
     const int gr = r0 + r;
@@ -196,15 +218,19 @@ __global__ void __launch_bounds__(256) qr_step_kernel(QrArgs a, int k, int iter)
   if (b == 0) {
     const double eta = deficient ? 0.0 : (g / rho) / rho;  // beta / rho, beta = q^T rhs = g / rho
     // w = Rinv[0:j, 0:j] (c1 + c2)
-    for (int i = tid; i < j; i += BT) {
+    // (R^{-1} is stored row-major: a warp reads row i contiguously)
+    for (int i = warp; i < j; i += nwarps) {
+      const double* Ri = a.Rinv + (long long)i * a.kmax;
       double s = 0.0;
-      #pragma unroll 8
-      for (int l = i; l < j; ++l) s = fma(a.Rinv[(long long)l * a.kmax + i], c1s[l] + cv[l], s);
-      const double yi = a.y[i] - eta * s;
-      a.Rinv[(long long)j * a.kmax + i] = deficient ? 0.0 : -s / rho;
-      a.y[i] = yi;
-      a.Yhist[(long long)j * a.kmax + i] = yi;
-      wv[i] = -s;
+      for (int l = i + lane; l < j; l += 32) s = fma(Ri[l], c1s[l] + cv[l], s);
+      s = warp_sum(s);
+      if (lane == 0) {
+        const double yi = a.y[i] - eta * s;
+        a.Rinv[(long long)i * a.kmax + j] = deficient ? 0.0 : -s / rho;
+        a.y[i] = yi;
+        a.Yhist[(long long)j * a.kmax + i] = yi;
+        wv[i] = -s;
+      }
     }
     if (tid == 0) {
       a.Rinv[(long long)j * a.kmax + j] = deficient ? 0.0 : 1.0 / rho;
@@ -269,21 +295,20 @@ __global__ void __launch_bounds__(256) qr_step_kernel(QrArgs a, int k, int iter)
   double* ys = cv;
   for (int i = tid; i <= j; i += BT) ys[i] = __ldcg(&a.Yhist[(long long)j * a.kmax + i]);
   __syncthreads();
+  const int ell = a.ell;
+  const double *Zm = a.Z, *Fm = a.F;
+  split_rows(nr, j + 1, ys, [&](int i, int r) {
+    const int gr = r0 + r;
+    return gr < ell ? Zm[(long long)i * ell + gr] : Fm[(long long)i * ell + gr - ell];
+  }, red, mv);
   double s_top = 0.0, s_bot = 0.0;
   for (int r = tid; r < nr; r += BT) {
     const int gr = r0 + r;
     if (gr < a.ell) {
-      double s = 0.0;
-      #pragma unroll 8
-      for (int i = 0; i <= j; ++i) s = fma(a.Z[(long long)i * a.ell + gr], ys[i], s);
-      const double d = s - a.sr0[gr];
+      const double d = mv[r] - a.sr0[gr];
       s_top = fma(d, d, s_top);
     } else {
-      const int fr = gr - a.ell;
-      double s = 0.0;
-      #pragma unroll 8
-      for (int i = 0; i <= j; ++i) s = fma(a.F[(long long)i * a.ell + fr], ys[i], s);
-      s_bot = fma(s, s, s_bot);
+      s_bot = fma(mv[r], mv[r], s_bot);
     }
   }
   s_top = block_sum(s_top, scratch);
@@ -302,6 +327,24 @@ __global__ void __launch_bounds__(256) qr_step_kernel(QrArgs a, int k, int iter)
     a.sres[j] = sqrt(st);
     a.proj[j] = sqrt(st + a.lam * a.lam * sb);
   }
+}
+
+// Launch one projected-solve step (cooperative grid: the five phase barriers
+// are grid-wide).  Measured: the same kernel as one 16-CTA thread-block
+// cluster (hardware cluster barriers) was no faster in isolation (61 vs 58 us
+// per step at config 2 -- the phases are latency chains, not barrier-bound)
+// and slower inside the config-4 solve (fewer CTAs, and a 16-SM cluster slot
+// is harder to find beside the SpMV).
+inline cudaError_t launch_qr_step(const QrArgs& qa, int k, int iter, int NB, size_t smem, cudaStream_t s) {
+  QrArgs a = qa;
+  void* args[] = {&a, &k, &iter};
+  return cudaLaunchCooperativeKernel((void*)qr_step_kernel, dim3(NB), dim3(256), args, smem, s);
+}
+
+// kernel attributes for a step with `smem` bytes of dynamic shared memory
+inline cudaError_t prepare_qr_step(size_t smem) {
+  if (smem <= 48 * 1024) return cudaSuccess;
+  return cudaFuncSetAttribute(qr_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
 }  // namespace hs
