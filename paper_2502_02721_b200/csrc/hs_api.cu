@@ -1675,8 +1675,14 @@ int hs_ctx_create(int device, hs_ctx** out) {
     CK(cudaSetDevice(device));
     auto* c = new hs_ctx();
     c->device = device;
-    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+    // the main stream carries the basis recurrence (the critical path); the aux
+    // stream (sketches, projected solves) gets the lower priority, so its blocks
+    // only take SM slots the main stream's pending kernels do not claim
+    int prio_lo = 0, prio_hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    if (env_flag("HS_FLAT_PRIO")) prio_lo = prio_hi = 0;
+    CK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi));
+    CK(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, prio_lo));
     if (device < 64 && !g_dev_stream[device]) {
       // keep freed blocks in the device pool (no release back to the driver)
       cudaMemPool_t pool;
