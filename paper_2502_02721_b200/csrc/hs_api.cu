@@ -848,6 +848,8 @@ struct hs_result {
   double loop_ms = 0.0;
   // device-resident bases kept for on-demand export
   std::shared_ptr<DBuf> Lb, Db;
+  // final iterate on the device (n doubles), when the solver keeps it there instead of in x
+  std::shared_ptr<DBuf> xdev;
   long long ldn = 0, ldm = 0;
   hs_ctx* ctx = nullptr;
   // sharded solves keep only this rank's rows of the bases
@@ -983,7 +985,11 @@ struct Solver {
     std::shared_ptr<DBuf> Db;
     if (!square) Db = std::make_shared<DBuf>((size_t)(K + 2) * ldm * sizeof(B));
     DBuf u(ldm * sizeof(T)), q(ldn * sizeof(T)), r0(ldm * sizeof(T)), bT(ldm * sizeof(T));
-    DBuf bd(m * sizeof(double), false), x0d, xtd, xd(n * sizeof(double));
+    DBuf bd(m * sizeof(double), false), x0d, xtd;
+    // x stays on the device with the result; hs_result_x copies it straight
+    // into the caller's array (no host staging vector)
+    auto xdp = std::make_shared<DBuf>(n * sizeof(double));
+    DBuf& xd = *xdp;
     DBuf Hb((size_t)(K + 1) * K * sizeof(double)), Wb((size_t)(K + 2) * (K + 1) * sizeof(double));
     DBuf PD((size_t)ldp * ldp * sizeof(T)), PL((size_t)ldp * ldp * sizeof(T));
     DBuf tpos(ldp * sizeof(long long)), gpos(ldp * sizeof(long long));
@@ -1549,9 +1555,9 @@ struct Solver {
     const auto t_events = now();
 
     // ---- copy back
-    CK(cudaMemcpyAsync(xstage, xd.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    res->x.assign(xstage, xstage + n);
+    (void)xstage;
+    res->xdev = xdp;
     const auto t_xcopy = now();
     res->sres.resize(kend);
     res->proj.resize(kend);
