@@ -479,8 +479,18 @@ struct hs_op {
   long long psf_row0 = 0, psf_rows = 0;
   mutable DBuf psfwin;
 
+  // tomography A^T input staged by the caller in the blocked sinogram layout
+  // (the loop's normalize kernel writes it beside d_{k+1}); null if the
+  // operator does not gather from a blocked sinogram
+  void* blocked_input(size_t elem_bytes) const {
+    if (kind != OP_CSR || sblk.n_bins <= 0 || Ats.nslices <= 0) return nullptr;
+    const size_t need = (size_t)sblk.size(n_angles) * elem_bytes;
+    if (yB.bytes < need) yB.alloc(need, false);
+    return yB.p;
+  }
+
   template <class V, class Tin, class T>
-  void apply_t(const void* x, void* y, bool transpose) const {
+  void apply_t(const void* x, void* y, bool transpose, bool preblocked = false) const {
     cudaStream_t s = ctx->stream;
     const Tin* xi = reinterpret_cast<const Tin*>(x);
     T* yo = reinterpret_cast<T*>(y);
@@ -493,7 +503,9 @@ struct hs_op {
                            (double)M.n_exc * 4 + (double)M.nslices * 8 + (double)M.cols * sizeof(Tin) +
                            (double)M.rows * sizeof(T);
       const bool tflag = !transpose && sflag.p != nullptr;
-      if (transpose && sblk.n_bins > 0) {
+      if (transpose && sblk.n_bins > 0 && preblocked) {
+        xi = yB.as<Tin>();
+      } else if (transpose && sblk.n_bins > 0) {
         Prof p(ctx, "y_block", 2.0 * (double)m * sizeof(Tin));
         const size_t need = (size_t)sblk.size(n_angles) * sizeof(Tin);
         if (yB.bytes < need) yB.alloc(need, false);
@@ -662,18 +674,19 @@ struct hs_op {
   }
 
   // x: type xdt; y: type T (wdt)
-  void apply(const void* x, int xdt, void* y, int wdt, bool transpose) const {
+  void apply(const void* x, int xdt, void* y, int wdt, bool transpose, bool preblocked = false) const {
+    const bool pb = preblocked;
     if (wdt == HS_F64) {
       if (xdt != HS_F64) fail(HS_ERR_TYPE, "fp64 work needs fp64 input vectors");
-      if (vdtype == HS_F64) apply_t<double, double, double>(x, y, transpose);
-      else apply_t<float, double, double>(x, y, transpose);
+      if (vdtype == HS_F64) apply_t<double, double, double>(x, y, transpose, pb);
+      else apply_t<float, double, double>(x, y, transpose, pb);
     } else if (wdt == HS_F32) {
       if (xdt == HS_F32) {
-        if (vdtype == HS_F64) apply_t<double, float, float>(x, y, transpose);
-        else apply_t<float, float, float>(x, y, transpose);
+        if (vdtype == HS_F64) apply_t<double, float, float>(x, y, transpose, pb);
+        else apply_t<float, float, float>(x, y, transpose, pb);
       } else if (xdt == HS_BF16) {
-        if (vdtype == HS_F64) apply_t<double, __nv_bfloat16, float>(x, y, transpose);
-        else apply_t<float, __nv_bfloat16, float>(x, y, transpose);
+        if (vdtype == HS_F64) apply_t<double, __nv_bfloat16, float>(x, y, transpose, pb);
+        else apply_t<float, __nv_bfloat16, float>(x, y, transpose, pb);
       } else {
         fail(HS_ERR_TYPE, "fp32 work needs fp32/bf16 input vectors");
       }
@@ -1396,11 +1409,15 @@ struct Solver {
         if (!skd)
           CK(cudaMemcpyAsync(Zb.as<double>() + (long long)(k - 1) * ell, Hcol(k - 1), (size_t)(k + 1) * sizeof(double),
                              cudaMemcpyDeviceToDevice, s));
-        normalize_kernel<T, B><<<grid_for(ldm, 256, NORM_G), 256, 0, s>>>(m, ldm, uel, pv.as<T>(), Dcol(k), st, 0, k);
+        // d_{k+1}, and the same values in the blocked sinogram layout A^T gathers from
+        B* ybk = reinterpret_cast<B*>(op->blocked_input(sizeof(B)));
+        if (env_flag("HS_NO_YB_FUSE")) ybk = nullptr;
+        normalize_kernel<T, B><<<grid_for(ldm, 256, NORM_G), 256, 0, s>>>(m, ldm, uel, pv.as<T>(), Dcol(k), st, 0, k,
+                                                                          op->sblk, ybk);
         CKL();
         if (defer_sk) sketch_u();
         if (sb) S2->apply(Dcol(k), bdt, Gb.as<double>() + (long long)k * ell);
-        op->apply(Dcol(k), bdt, q.p, wdt, true);
+        op->apply(Dcol(k), bdt, q.p, wdt, true, ybk != nullptr);
         // printed variant: F column k = S1 q before the elimination (solvers.py:488-490)
         if (printed) S1->apply(q.p, wdt, Fb.as<double>() + (long long)k * ell);
         fsub(q.as<T>(), gpos.as<long long>(), PL.as<T>(), ldp, k, k, 1, cvec.as<T>(), Wcol(k));

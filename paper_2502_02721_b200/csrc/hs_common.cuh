@@ -185,4 +185,15 @@ __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float& n0, fl
   n1 = r * s;
 }
 
+// Blocked sinogram layout for the A^T gathers (hs_ops.cuh):
+// one 128-byte line holds ab angles x bb bins.
+struct SinoBlk {
+  int n_bins, ab, bb, nbb;  // nbb = bin blocks per angle block
+  __host__ __device__ long long map(long long c) const {
+    const long long a = c / n_bins, b = c - a * n_bins;
+    return ((a / ab) * nbb + b / bb) * (ab * bb) + (a % ab) * bb + (b % bb);
+  }
+  __host__ __device__ long long size(long long n_angles) const { return ((n_angles + ab - 1) / ab) * nbb * ab * bb; }
+};
+
 }  // namespace hs

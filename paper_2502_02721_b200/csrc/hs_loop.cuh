@@ -305,12 +305,16 @@ __global__ void pivot_commit_kernel(int k, long long dim, double* __restrict__ h
 template <class T, class B>
 __global__ void __launch_bounds__(256)
 normalize_kernel(long long n, long long n_pad, const T* __restrict__ u, const T* __restrict__ pivval,
-                 B* __restrict__ dst, const LoopState* __restrict__ st, int side, int iter) {
+                 B* __restrict__ dst, const LoopState* __restrict__ st, int side, int iter,
+                 SinoBlk blk = SinoBlk{0, 0, 0, 0}, B* __restrict__ yb = nullptr) {
   if (st->bd_iter != 0 && st->bd_iter <= iter) return;
   const T p = *pivval;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n_pad;
        e += (long long)gridDim.x * blockDim.x) {
-    dst[e] = (e < n) ? cvt<B>(Rn<T>::div(u[e], p)) : cvt<B>(T(0));
+    const B v = (e < n) ? cvt<B>(Rn<T>::div(u[e], p)) : cvt<B>(T(0));
+    dst[e] = v;
+    // the next A^T apply's input, already in the blocked sinogram layout
+    if (yb != nullptr && e < n) yb[blk.map(e)] = v;
   }
 }
 

@@ -403,14 +403,7 @@ __global__ void __launch_bounds__(256) image_transpose_kernel(int grid, const Ti
 // one gather touches ~16 lines.  In the blocked layout a 128-byte line holds an
 // (ab angles x bb bins) block, and the same gather touches ~9 lines
 // (tools/ab_spmv.py; the sum order is unchanged, only the gather address).
-struct SinoBlk {
-  int n_bins, ab, bb, nbb;  // nbb = bin blocks per angle block
-  __host__ __device__ long long map(long long c) const {
-    const long long a = c / n_bins, b = c - a * n_bins;
-    return ((a / ab) * nbb + b / bb) * (ab * bb) + (a % ab) * bb + (b % bb);
-  }
-  __host__ __device__ long long size(long long n_angles) const { return ((n_angles + ab - 1) / ab) * nbb * ab * bb; }
-};
+// SinoBlk (the blocked sinogram layout) lives in hs_common.cuh
 
 __global__ void sino_block_cols_kernel(long long n, SinoBlk B, int* __restrict__ col) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
