@@ -62,8 +62,20 @@ struct QrArgs {
 inline int qr_blocks(int Ls) { return Ls < 48 ? 1 : (Ls + 47) / 48 < 64 ? (Ls + 47) / 48 : 64; }
 
 // dynamic shared memory of qr_step_kernel
-inline size_t qr_smem_bytes(int Ls, int NB, int kmax) {
+// The block's slice of Q (RS rows x the kmax columns, fp64) is staged in
+// shared memory at the start of every step when it fits (configs 1-5: 36-115
+// KB), so the Gram-Schmidt passes read it from shared memory instead of
+// walking L2 round trips column after column.
+constexpr size_t QR_SMEM_CAP = 200 * 1024;
+__host__ __device__ inline size_t qr_smem_base(int Ls, int NB, int kmax) {
   return (2 * (size_t)((Ls + NB - 1) / NB) + 4 * (size_t)kmax + 256) * sizeof(double);
+}
+__host__ __device__ inline bool qr_q_in_smem(int Ls, int NB, int kmax) {
+  return qr_smem_base(Ls, NB, kmax) + (size_t)((Ls + NB - 1) / NB) * kmax * sizeof(double) <= QR_SMEM_CAP;
+}
+inline size_t qr_smem_bytes(int Ls, int NB, int kmax) {
+  return qr_smem_base(Ls, NB, kmax) +
+         (qr_q_in_smem(Ls, NB, kmax) ? (size_t)((Ls + NB - 1) / NB) * kmax * sizeof(double) : 0);
 }
 
 // out[i] = sum_{r < nr} Q[i*ldq + r] * v[r] for i < j: one warp per column,
@@ -148,6 +160,20 @@ __global__ void __launch_bounds__(256) qr_step_kernel(QrArgs a, int k, int iter)
   double* gv = wv + a.kmax;   // kmax (projection coefficients)
   double* red = gv + a.kmax;  // 256 (split_rows partials)
   double* mv = red + 256;     // RS (split_rows results)
+  // this block's rows of Q: shared memory (column i at Qs[i * RS]) or global
+  const bool qsm = qr_q_in_smem(a.Ls, NB, a.kmax);
+  double* Qs = mv + RS;
+  if (qsm) {
+    const unsigned sbase = (unsigned)__cvta_generic_to_shared(Qs);
+    for (int idx = tid; idx < j * nr; idx += BT) {
+      const int i = idx / nr, r = idx - i * nr;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sbase + (unsigned)((i * RS + r) * 8)),
+                   "l"(a.Q + (long long)i * a.ldq + r0 + r));
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+  }
+  const double* Qb = qsm ? Qs : a.Q + r0;
+  const long long ldq = qsm ? RS : a.ldq;
   __shared__ double scratch[32];
 
   // phase 1: load the new stacked column, partial Q^T a
@@ -156,7 +182,7 @@ __global__ void __launch_bounds__(256) qr_step_kernel(QrArgs a, int k, int iter)
     av[r] = gr < a.ell ? a.zcol[gr] : a.lam * a.fcol[gr - a.ell];
   }
   __syncthreads();
-  block_dots(a.Q + r0, a.ldq, j, av, nr, P1 + (long long)b * pld);
+  block_dots(Qb, (int)ldq, j, av, nr, P1 + (long long)b * pld);
   grid.sync();
 
   // phase 2: c1 = sum_b P1;  a -= Q c1;  partial Q^T a
@@ -168,12 +194,10 @@ __global__ void __launch_bounds__(256) qr_step_kernel(QrArgs a, int k, int iter)
     c1s[i] = s;
   }
   __syncthreads();
-  const double* Qb = a.Q + r0;
-  const long long ldq = a.ldq;
   split_rows(nr, j, cv, [&](int i, int r) { return Qb[(long long)i * ldq + r]; }, red, mv);
   for (int r = tid; r < nr; r += BT) av[r] -= mv[r];
   __syncthreads();
-  block_dots(a.Q + r0, a.ldq, j, av, nr, P2 + (long long)b * pld);
+  block_dots(Qb, (int)ldq, j, av, nr, P2 + (long long)b * pld);
   grid.sync();
 
   // phase 3: c2 = sum_b P2;  a -= Q c2;  partial |a|^2 and a^T rhs
@@ -219,17 +243,26 @@ __global__ void __launch_bounds__(256) qr_step_kernel(QrArgs a, int k, int iter)
     const double eta = deficient ? 0.0 : (g / rho) / rho;  // beta / rho, beta = q^T rhs = g / rho
     // w = Rinv[0:j, 0:j] (c1 + c2)
     // (R^{-1} is stored row-major: a warp reads row i contiguously)
-    for (int i = warp; i < j; i += nwarps) {
-      const double* Ri = a.Rinv + (long long)i * a.kmax;
-      double s = 0.0;
-      for (int l = i + lane; l < j; l += 32) s = fma(Ri[l], c1s[l] + cv[l], s);
-      s = warp_sum(s);
-      if (lane == 0) {
-        const double yi = a.y[i] - eta * s;
-        a.Rinv[(long long)i * a.kmax + j] = deficient ? 0.0 : -s / rho;
-        a.y[i] = yi;
-        a.Yhist[(long long)j * a.kmax + i] = yi;
-        wv[i] = -s;
+    // four rows per warp pass, so their loads are in flight together
+    for (int i0 = warp * 4; i0 < j; i0 += nwarps * 4) {
+      double sr[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int l = i0 + lane; l < j; l += 32) {
+        const double cl = c1s[l] + cv[l];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (i0 + u < j && l >= i0 + u) sr[u] = fma(a.Rinv[(long long)(i0 + u) * a.kmax + l], cl, sr[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u;
+        const double sv = warp_sum(sr[u]);
+        if (lane == 0 && i < j) {
+          const double yi = a.y[i] - eta * sv;
+          a.Rinv[(long long)i * a.kmax + j] = deficient ? 0.0 : -sv / rho;
+          a.y[i] = yi;
+          a.Yhist[(long long)j * a.kmax + i] = yi;
+          wv[i] = -sv;
+        }
       }
     }
     if (tid == 0) {
