@@ -42,6 +42,17 @@ METRIC = "sketched-LSLU iterations/sec at 2048^2 tomography; achieved HBM GB/s"
 UNIT = "iterations/s"
 
 
+# BASELINE.json's configs (paper_2502_02721_b200.problems.CONFIGS; restated here so the
+# reference arm names its workload without importing the device package)
+WORKLOADS = {
+    1: "1D deblurring, dense fp64 1024^2 Toeplitz (sigma=0.02 n), sCMRH K=100, Gaussian s=400",
+    2: "2D deblurring 256^2, 15x15 PSF (sigma=2), fp32, sCMRH K=200, Gaussian s=800",
+    3: "tomography 512^2, 180 angles x 725 bins, CSR fp32, sLSLU lam=1e-3 K=200, sparse-sign s=800 zeta=8",
+    4: "tomography 2048^2, 720 angles x 2897 bins, CSR fp32, sLSLU K=300, sparse-sign s=1200 zeta=8",
+    5: "deblurring 4096^2, 31x31 PSF (sigma=4), bf16 basis / fp32 work, sCMRH K=150, Gaussian s=600",
+}
+
+
 def _traffic(args):
     """DRAM bytes per SpMV launch from the committed ncu capture (config 4 only)."""
     if args.config != 4 or args.scale:
@@ -146,7 +157,7 @@ def run_ours(args, ws, rank, local):
 
     import paper_2502_02721_b200 as hs
     from paper_2502_02721_b200 import _lib
-    from paper_2502_02721_b200.problems import CONFIGS, make_workload
+    from paper_2502_02721_b200.problems import make_workload
 
     os.environ["HS_DEVICE"] = str(local)
     _lib.load()
@@ -220,7 +231,7 @@ def run_ours(args, ws, rank, local):
         "dtype": "f32",
         "data": "synthetic (seeded random-ellipse phantom, 1% noise; device-built exact-chord operator)",
         "config": {
-            "workload": f"cfg{args.config}: " + CONFIGS[args.config],
+            "workload": f"cfg{args.config}: " + WORKLOADS[args.config],
             "grid": w.meta.get("grid"), "angles": w.meta.get("angles"), "bins": w.meta.get("bins"),
             "nnz": inf.get("nnz"), "maxiter": K, "sketch": "sparse-sign ell=%d zeta=8" % w.cfg.sketch_rows,
             "step": "one full sLSLU solve (maxiter iterations)",
@@ -294,7 +305,14 @@ def run_reference(args, ws, rank):
     return {
         "metric": METRIC, "impl": "reference", "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": {"workload": f"cfg{args.config}", "sample": last["sample"] if last else None},
+        "data": "synthetic",
+        # the same workload description as the device arm's line
+        "config": {"workload": f"cfg{args.config}: " + WORKLOADS[args.config], "grid": grid, "angles": angles,
+                   "bins": bins, "nnz": last.get("nnz") if last else None, "maxiter": K,
+                   "sketch": "sparse-sign ell=%d zeta=8" % w.cfg.sketch_rows,
+                   "step": "one full sLSLU solve (maxiter iterations; CPU: bounded sample, rate extrapolated)",
+                   "l2": "inputs (A + A^T) far larger than L2; no flush", "parallelism": "single (host threads)",
+                   "sample": last["sample"] if last else None},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": last["cores"] if last else None, "kind": "port",
                          "sample": last["sample"] if last else None},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

@@ -145,6 +145,7 @@ def run(w, budget_s=20.0, nthreads=None, b=None):
         "unit": "iterations/s",
         "cores": nthreads,
         "kind": "port",
+        "nnz": int(A[0][-1]),
         "sample": (f"oracle/coracle.c (C port of solvers.py:410-539, fp32 vectors, OpenMP) on the full "
                    f"{meta['grid']}^2 x {meta['angles']}x{meta['bins']} operator ({int(A[0][-1])} nnz, host-built): "
                    f"{r['done']} of {K} iterations in {sum(r['iter_s']):.1f}s, rate extrapolated to {K} iterations "

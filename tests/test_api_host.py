@@ -96,3 +96,12 @@ def test_python_callable_operator_has_no_device_path():
         hs.to_device_operator(A)
     with pytest.raises(ValueError):
         A.apply(np.ones(4))
+
+
+def test_bench_workload_names_match_configs():
+    """bench.py's reference arm names its workload without importing the device
+    package; the strings must stay those of problems.CONFIGS."""
+    import bench
+    from paper_2502_02721_b200.problems import CONFIGS
+
+    assert bench.WORKLOADS == CONFIGS

@@ -39,5 +39,24 @@ for cid in ids:
         "sres_last": r.trace.final().sres_norm, "rank_fallback": any(r.trace.column("rank_fallback")),
         "kernels_ms": {k: round(v["ms"], 2) for k, v in sorted(stats.items(), key=lambda kv: -kv[1]["ms"])},
     }
+    if cid == 5:
+        # BASELINE config 5: "compared against an fp32-storage run" -- same problem,
+        # basis stored in fp32 instead of bf16
+        import dataclasses
+        r32 = solve(w.operator, w.b, dataclasses.replace(w.cfg, basis_dtype="float32"), x_true=w.x_true,
+                    sketch=w.sketch)
+        t16, t32 = r.factorization.t, r32.factorization.t
+        nt = min(len(t16), len(t32))
+        diff = np.nonzero(t16[:nt] != t32[:nt])[0]
+        rel32 = r32.trace.column("rel_err")
+        out["fp32_storage"] = {
+            "it_per_s": round(len(r32.trace.records) / (r32.loop_ms / 1e3), 1),
+            "rel_err_first_min_last": [round(rel32[0], 5), round(min(rel32), 5), round(rel32[-1], 5)],
+            "rel_err_min_bf16_over_fp32": round(min(rel) / min(rel32), 4),
+            "first_pivot_divergence_k": int(diff[0]) + 1 if len(diff) else None,
+        }
+        kmin = int(np.argmin(rel32))
+        out["fp32_storage"]["argmin_rel_err_k"] = [int(np.argmin(rel)) + 1, kmin + 1]
+        del r32
     print(json.dumps(out), flush=True)
     del r, w
