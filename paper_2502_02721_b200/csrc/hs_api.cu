@@ -959,11 +959,7 @@ struct Solver {
             double* hcol) {
     if (k == 0) return;
     cudaStream_t s = ctx->stream;
-    if (k <= 64) {
-      fsub_warp_kernel<T, 2><<<1, 32, 0, s>>>(u, pos, 0, P, ldp, nullptr, k, st, iter, side, c, hcol);
-    } else {
-      fsub_block_kernel<T><<<1, 512, (size_t)k * sizeof(T), s>>>(u, pos, 0, P, ldp, k, st, iter, side, c, hcol);
-    }
+    launch_fsub<T>(s, u, pos, P, ldp, k, st, iter, side, c, hcol);
     CKL();
   }
 

@@ -123,6 +123,104 @@ fsub_block_kernel(const T* __restrict__ u, const long long* __restrict__ pos, lo
   }
 }
 
+// Panel version (the default): the same blocked sequence, with P read from
+// shared memory.  Panel b (columns b0..b0+31 of P, rows b0..k-1) is copied by
+// cp.async while panel b-1 is being used, so the solve walks shared memory
+// instead of one L2 round trip per diagonal block and per trailing update
+// (config 2: ~21 us -> see DESIGN.md).  Per row the operations and their
+// order are those of fsub_block_kernel: bit-identical.
+template <class T>
+__device__ __forceinline__ void fsub_panel_copy(const T* __restrict__ P, int ldp, int b0, int k, T* dst) {
+  const int W = k - b0;
+  const int nb = min(32, W);
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(dst);
+  for (int idx = threadIdx.x; idx < nb * W; idx += blockDim.x) {
+    const int o = idx / W, jj = idx - o * W;
+    const T* src = P + (long long)(b0 + o) * ldp + b0 + jj;
+    if (sizeof(T) == 8)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sbase + (unsigned)(idx * 8)), "l"(src));
+    else
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sbase + (unsigned)(idx * 4)), "l"(src));
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
+inline size_t fsub_panel_smem(int k, size_t tsize) { return ((size_t)k + 2 * 32 * (size_t)k) * tsize; }
+
+template <class T>
+__global__ void __launch_bounds__(256)
+fsub_panel_kernel(const T* __restrict__ u, const long long* __restrict__ pos, long long pos_offset,
+                  const T* __restrict__ P, int ldp, int k, const LoopState* __restrict__ st, int iter, int side,
+                  T* __restrict__ c, double* __restrict__ hcol) {
+  if (st->bd_iter != 0 && st->bd_iter < iter) return;
+  if (side == 1 && st->bd_iter == iter) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* v = reinterpret_cast<T*>(smem_raw);  // k values
+  T* pan[2] = {v + k, v + k + 32 * k};    // two panels of <= 32 x k
+  const int nbt = (k + 31) / 32;
+  fsub_panel_copy<T>(P, ldp, 0, k, pan[0]);
+  for (int j = threadIdx.x; j < k; j += blockDim.x) v[j] = u[pos[j] - pos_offset];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int b = 0; b < nbt; ++b) {
+    const int b0 = b * 32, nb = min(32, k - b0), W = k - b0;
+    if (b + 1 < nbt) {
+      fsub_panel_copy<T>(P, ldp, b0 + 32, k, pan[(b + 1) & 1]);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    const T* pn = pan[b & 1];  // pn[o * W + (j - b0)] = P[(b0 + o) * ldp + j]
+    if (warp == 0) {
+      const int j = b0 + lane;
+      T vj = lane < nb ? v[j] : T(0);
+#pragma unroll
+      for (int o = 0; o < 32; ++o) {
+        if (o < nb) {
+          const T co = __shfl_sync(0xffffffffu, vj, o);
+          if (lane > o && lane < nb) vj = Rn<T>::sub(vj, Rn<T>::mul(co, pn[o * W + lane]));
+        }
+      }
+      if (lane < nb) {
+        v[j] = vj;
+        c[j] = vj;
+        hcol[j] = (double)vj;
+      }
+    }
+    __syncthreads();
+    for (int j = b0 + nb + threadIdx.x; j < k; j += blockDim.x) {
+      T vj = v[j];
+      for (int o = 0; o < nb; ++o) vj = Rn<T>::sub(vj, Rn<T>::mul(v[b0 + o], pn[o * W + (j - b0)]));
+      v[j] = vj;
+    }
+    __syncthreads();
+  }
+}
+
+// forward substitution for k pivot rows (one CTA); every call site goes through here
+template <class T>
+inline void launch_fsub(cudaStream_t s, const T* u, const long long* pos, const T* P, int ldp, int k,
+                        const LoopState* st, int iter, int side, T* c, double* hcol) {
+  if (k <= 0) return;
+  const size_t smem = fsub_panel_smem(k, sizeof(T));
+  static const bool legacy = [] {
+    const char* e = getenv("HS_FSUB_LEGACY");  // A/B knob: the register-blocked kernels below
+    return e && *e && *e != '0';
+  }();
+  if (smem <= 200 * 1024 && !legacy) {
+    static size_t attr = 48 * 1024;  // per instantiation
+    if (smem > attr) {
+      cudaFuncSetAttribute(fsub_panel_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = 200 * 1024;
+    }
+    fsub_panel_kernel<T><<<1, 256, smem, s>>>(u, pos, 0, P, ldp, k, st, iter, side, c, hcol);
+  } else if (k <= 64) {
+    fsub_warp_kernel<T, 2><<<1, 32, 0, s>>>(u, pos, 0, P, ldp, nullptr, k, st, iter, side, c, hcol);
+  } else {
+    fsub_block_kernel<T><<<1, 512, (size_t)k * sizeof(T), s>>>(u, pos, 0, P, ldp, k, st, iter, side, c, hcol);
+  }
+}
+
 // --------------------------------------------------------------------------
 // vector load helpers for the basis pass
 template <class B, int VEC> struct VecLoad;
