@@ -539,8 +539,12 @@ struct hs_op {
         int gshift = -1;
         if (img_grid > 0 && (img_grid & (img_grid - 1)) == 0) gshift = __builtin_ctz((unsigned)img_grid);
         // few slices (< 2 per resident warp): the walk is latency-bound, use the deeper pipeline
+        // -- but not for long rows (one rank's share of config 4 on 8 GPUs: 8.1k
+        // slices of ~460 chunks; depth 0 at full occupancy 0.52 ms, depth 1 0.68 ms,
+        // tools/ab_rank_share.py)
+        const long long avg_chunks = M.nslices > 0 ? M.slots / (M.nslices * 128) : 0;
         const bool deep = env_flag("HS_D16_DEEP") ||
-                          (M.nslices < 2LL * ctx->num_sms * 48 && !env_flag("HS_D16_SHALLOW"));
+                          (M.nslices < 2LL * ctx->num_sms * 48 && avg_chunks < 256 && !env_flag("HS_D16_SHALLOW"));
         const bool p2 = gshift >= 0 || !tflag;
         // pipeline depth in chunks per gather step (HS_D16_PIPE overrides for A/B runs)
         // (fewer slices than ~32 per SM, e.g. config 3's A: 4,078 slices of 460-entry rays: depth 2,

@@ -1,5 +1,6 @@
-"""Config 5 (or 2) through the row-sharded sCMRH loop forced on one rank, beside the
-single-GPU loop (same problem): it/s of both and bitwise agreement of the pivots.
+"""A config (5, 2: sCMRH on the PSF operator; 3, 4: sLSLU on tomography) through the
+row-sharded loop forced on one rank, beside the single-GPU loop (same problem):
+it/s of both and bitwise agreement of the pivots.
 
     python tools/run_sharded_single.py [CFG]
 """
@@ -20,8 +21,9 @@ res = {}
 for tag, forced in (("single", False), ("sharded_p1", True)):
     hsd.force_sharding(forced)
     w = make_workload(cid)
-    r = hs.scmrh(w.operator, w.b, w.cfg, x_true=w.x_true, sketch=w.sketch)  # warm
-    r = hs.scmrh(w.operator, w.b, w.cfg, x_true=w.x_true, sketch=w.sketch)
+    solve = hs.slslu if w.solver == "slslu" else hs.scmrh
+    r = solve(w.operator, w.b, w.cfg, x_true=w.x_true, sketch=w.sketch)  # warm
+    r = solve(w.operator, w.b, w.cfg, x_true=w.x_true, sketch=w.sketch)
     res[tag] = r
     out[tag + "_it_per_s"] = round(len(r.trace.records) / (r.loop_ms / 1e3), 1)
     del w
