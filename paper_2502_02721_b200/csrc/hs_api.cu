@@ -549,7 +549,9 @@ struct hs_op {
         // pipeline depth in chunks per gather step (HS_D16_PIPE overrides for A/B runs)
         // (fewer slices than ~32 per SM, e.g. config 3's A: 4,078 slices of 460-entry rays: depth 2,
         // 0.157 -> 0.107 ms; its A^T, 8,192 shorter slices, stays at depth 1: 0.091 vs 0.106 ms)
-        int depth = deep ? (M.nslices < 32LL * ctx->num_sms ? 2 : 1) : 0;
+        // between 32 and 96 slices per SM (config 3's A^T: 8,192 slices of 57 chunks) the
+        // stream goes through the per-lane cp.async ring: 0.090 -> 0.080 ms (depth 1)
+        int depth = deep ? (M.nslices < 32LL * ctx->num_sms ? 2 : 8) : 0;
         if (const char* e = getenv("HS_D16_PIPE")) depth = atoi(e);
         auto pick = [&](auto p2c) {
           constexpr bool P2 = decltype(p2c)::value;
@@ -558,6 +560,22 @@ struct hs_op {
                : depth == 1 ? sell_spmv_d16_kernel<V, Tin, T, P2, 1>
                             : sell_spmv_d16_kernel<V, Tin, T, P2, 0>;
         };
+        if (depth == 8) {
+          // per-lane cp.async ring (hs_ops.cuh: sell_spmv_d16_ring_kernel)
+          constexpr bool F32 = sizeof(T) == 4 && sizeof(V) == 4;
+          constexpr int NS = 8, MINB = F32 ? 4 : 2;
+          auto rk = p2 ? sell_spmv_d16_ring_kernel<V, Tin, T, true, NS, MINB>
+                       : sell_spmv_d16_ring_kernel<V, Tin, T, false, NS, MINB>;
+          const int smem = D16Ring<V, NS>::smem_bytes(256);
+          if (smem > 48 * 1024) CK(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+          rk<<<grid, 256, smem, s>>>(M.rows, M.nslices, M.sptr.as<long long>(), M.rlen.as<int>(), M.rbase.as<int>(),
+                                     M.dcol.as<short>(), M.val.as<V>(), xi, tflag ? xT.as<Tin>() : nullptr,
+                                     tflag ? sflag.as<unsigned char>() : nullptr, img_grid, gshift >= 0 ? gshift : 0,
+                                     M.rperm.as<int>(), transpose ? nullptr : M.sorder.as<int>(),
+                                     M.sched.as<unsigned int>(), yo);
+          CKL();
+          return;
+        }
         auto kern = p2 ? pick(std::true_type{}) : pick(std::false_type{});
         kern<<<grid, 256, 0, s>>>(M.rows, M.nslices, M.sptr.as<long long>(), M.rlen.as<int>(), M.rbase.as<int>(),
                                   M.dcol.as<short>(), M.val.as<V>(), xi, tflag ? xT.as<Tin>() : nullptr,

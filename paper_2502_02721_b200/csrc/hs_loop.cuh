@@ -154,7 +154,7 @@ fsub_panel_kernel(const T* __restrict__ u, const long long* __restrict__ pos, lo
                   T* __restrict__ c, double* __restrict__ hcol) {
   if (st->bd_iter != 0 && st->bd_iter < iter) return;
   if (side == 1 && st->bd_iter == iter) return;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   T* v = reinterpret_cast<T*>(smem_raw);  // k values
   T* pan[2] = {v + k, v + k + 32 * k};    // two panels of <= 32 x k
   const int nbt = (k + 31) / 32;

@@ -1055,6 +1055,140 @@ __global__ void tile_perm_kernel(int grid, long long nslots, int* __restrict__ r
   rperm[slot] = (r < grid && c < grid) ? (int)(r * grid + c) : -1;
 }
 
+// ---- 16-bit deltas through a per-lane cp.async ring (latency-bound operators) ----
+// For operators with fewer slices than warp slots (config 3; one rank's share
+// of config 4 on 8 GPUs) the register-prefetched kernels keep ~25 KB of the
+// stream in flight per SM against the ~44 KB the HBM bandwidth-latency
+// product needs (ncu: 42-52% of DRAM bandwidth).  Here every lane copies its
+// own chunks' 8 B of deltas and 4 x sizeof(V) B of values by LDGSTS into an
+// NS-deep per-thread shared-memory ring (NS-1 chunks ahead, no registers
+// held), and decodes chunk q+1 and issues its gathers before adding chunk q.
+// Same products, same order of adds as d16_row: bit-identical.
+__device__ __forceinline__ void cpasync8(unsigned dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+
+template <class V, int NS>
+struct D16Ring {
+  static constexpr int VB = 4 * (int)sizeof(V);  // value bytes per lane per chunk
+  static constexpr int smem_bytes(int threads) { return NS * threads * (VB + 8); }
+};
+
+template <int GM, class V, class Tin, class T, int NS>
+__device__ __forceinline__ T d16_row_ring(const short* __restrict__ dp, const V* __restrict__ vp, int c, int len,
+                                          const Tin* __restrict__ x, int m, int sh, int grid, unsigned vs,
+                                          unsigned ds, unsigned VSTR, unsigned DSTR,
+                                          const unsigned char* __restrict__ vsp, const unsigned char* __restrict__ dsp) {
+  const int nq = (len + 3) >> 2;
+  auto issue = [&](int k, int slot) {
+    if (k < nq) {
+      cpasync16(vs + slot * VSTR, vp + (long long)k * 128, 0ull);
+      if (sizeof(V) == 8) cpasync16(vs + slot * VSTR + 16, vp + (long long)k * 128 + 2, 0ull);
+      cpasync8(ds + slot * DSTR, dp + (long long)k * 128);
+    }
+    cpasync_commit();
+  };
+#pragma unroll
+  for (int k = 0; k < NS - 1; ++k) issue(k, k);
+  T acc = T(0);
+  if (nq == 0) {
+    cpasync_wait<0>();
+    return acc;
+  }
+  // chunk 0: decode and gather
+  cpasync_wait<NS - 2>();
+  T g[4];
+  Chunk4<V> v;
+  {
+    const int2 d = *reinterpret_cast<const int2*>(dsp);
+    const int c0 = c + (int)(short)(d.x & 0xffff), c1 = c0 + (d.x >> 16);
+    const int c2 = c1 + (int)(short)(d.y & 0xffff), c3 = c2 + (d.y >> 16);
+    c = c3;
+    g[0] = gather_x<T>(x, gpos<GM>(c0, m, sh, grid));
+    g[1] = gather_x<T>(x, gpos<GM>(c1, m, sh, grid));
+    g[2] = gather_x<T>(x, gpos<GM>(c2, m, sh, grid));
+    g[3] = gather_x<T>(x, gpos<GM>(c3, m, sh, grid));
+    v = Chunk4<V>::lds(vsp);
+  }
+  for (int q = 0; q < nq; ++q) {
+    // refill the slot of chunk q-1 (consumed) with chunk q+NS-1
+    issue(q + NS - 1, (q + NS - 1) % NS);
+    T gn[4] = {T(0), T(0), T(0), T(0)};
+    Chunk4<V> vn = v;
+    if (q + 1 < nq) {
+      cpasync_wait<NS - 2>();  // chunk q+1 has landed
+      const int sl = (q + 1) % NS;
+      const int2 d = *reinterpret_cast<const int2*>(dsp + sl * DSTR);
+      const int c0 = c + (int)(short)(d.x & 0xffff), c1 = c0 + (d.x >> 16);
+      const int c2 = c1 + (int)(short)(d.y & 0xffff), c3 = c2 + (d.y >> 16);
+      c = c3;
+      gn[0] = gather_x<T>(x, gpos<GM>(c0, m, sh, grid));
+      gn[1] = gather_x<T>(x, gpos<GM>(c1, m, sh, grid));
+      gn[2] = gather_x<T>(x, gpos<GM>(c2, m, sh, grid));
+      gn[3] = gather_x<T>(x, gpos<GM>(c3, m, sh, grid));
+      vn = Chunk4<V>::lds(vsp + sl * VSTR);
+    }
+    const int nv = min(4, len - 4 * q);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (i < nv) acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[i]), g[i]));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) g[i] = gn[i];
+    v = vn;
+  }
+  cpasync_wait<0>();
+  return acc;
+}
+
+template <class V, class Tin, class T, bool POW2, int NS, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+sell_spmv_d16_ring_kernel(long long rows, long long nslices, const long long* __restrict__ sptr,
+                          const int* __restrict__ rlen, const int* __restrict__ rbase, const short* __restrict__ dcol,
+                          const V* __restrict__ val, const Tin* __restrict__ xrow, const Tin* __restrict__ xT,
+                          const unsigned char* __restrict__ sflag, int grid, int gshift, const int* __restrict__ rperm,
+                          const int* __restrict__ sorder, unsigned int* __restrict__ sched, T* __restrict__ y) {
+  using L = D16Ring<V, NS>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const unsigned VSTR = blockDim.x * L::VB, DSTR = blockDim.x * 8;
+  const unsigned vs = smem_u32(smem_raw) + threadIdx.x * L::VB;
+  const unsigned ds = smem_u32(smem_raw) + NS * VSTR + threadIdx.x * 8;
+  const unsigned char* vsp = smem_raw + threadIdx.x * L::VB;
+  const unsigned char* dsp = smem_raw + NS * VSTR + threadIdx.x * 8;
+  for (;;) {
+    unsigned int i = 0;
+    if (lane == 0) i = atomicAdd(&sched[0], 1u);
+    i = __shfl_sync(0xffffffffu, i, 0);
+    if (i >= nslices) break;
+    const long long s = sorder ? (long long)sorder[i] : (long long)i;
+    const bool tr = sflag != nullptr && sflag[s];
+    const long long slot = s * 32 + lane;
+    const long long row = rperm ? (long long)rperm[slot] : slot;
+    const int len = rlen[slot];
+    const int c = rbase[slot];
+    const long long base = sptr[s];
+    const short* dp = dcol + base + lane * 4;
+    const V* vp = val + base + lane * 4;
+    T acc;
+    if (!tr)
+      acc = d16_row_ring<0, V, Tin, T, NS>(dp, vp, c, len, xrow, 0, 0, grid, vs, ds, VSTR, DSTR, vsp, dsp);
+    else if (POW2)
+      acc = d16_row_ring<1, V, Tin, T, NS>(dp, vp, c, len, xT, grid - 1, gshift, grid, vs, ds, VSTR, DSTR, vsp, dsp);
+    else
+      acc = d16_row_ring<2, V, Tin, T, NS>(dp, vp, c, len, xT, 0, 0, grid, vs, ds, VSTR, DSTR, vsp, dsp);
+    if (row >= 0 && row < rows) y[row] = acc;
+  }
+  if (lane == 0) {
+    __threadfence();
+    const unsigned int done = atomicAdd(&sched[1], 1u);
+    if (done == gridDim.x * (blockDim.x >> 5) - 1) {
+      sched[0] = 0;
+      sched[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
 // ---- CSR -> SELL-32x4 conversion ------------------------------------------------
 // Slot s*32+lane holds row rperm[slot] (or row = slot without a permutation;
 // rperm < 0 marks an empty padding slot).  rlen is slot-indexed.
