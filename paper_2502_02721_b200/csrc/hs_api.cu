@@ -1269,6 +1269,8 @@ struct Solver {
     qa.rankfb = rfb.as<int>(); qa.st = st;
     DBuf Nnull((size_t)K * K * sizeof(double)), ndrop(sizeof(int));
     qa.Nnull = Nnull.as<double>(); qa.ndrop = ndrop.as<int>();
+    DBuf qdone(sizeof(unsigned int));  // zeroed; the reducing block resets it
+    qa.qdone = qdone.as<unsigned int>();
     const size_t qr_smem = qr_smem_bytes(Ls, NB, K);
     CK(prepare_qr_step(qr_smem));
     const bool rec_x = cfg.record_x && xt_h;

@@ -55,6 +55,7 @@ struct QrArgs {
   int* rankfb;          // kmax
   double* Nnull = nullptr;  // kmax x kmax: orthonormal null vectors of the dropped columns
   int* ndrop = nullptr;     // number of dropped columns so far
+  unsigned int* qdone = nullptr;  // arrival counter for the last-block residual reduction (null: grid barrier)
   LoopState* st;
 };
 
@@ -145,6 +146,7 @@ __global__ void __launch_bounds__(256) qr_step_kernel(QrArgs a, int k, int iter)
   const int NB = gridDim.x, b = blockIdx.x, tid = threadIdx.x, BT = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nwarps = BT >> 5;
   const int j = k - 1;  // new column index
+  const int d0 = *a.ndrop;  // read before block 0 can change it (phase 4, after three barriers)
   const int RS = (a.Ls + NB - 1) / NB;
   const int r0 = b * RS, r1 = min(a.Ls, r0 + RS);
   const int nr = max(0, r1 - r0);
@@ -239,7 +241,51 @@ __global__ void __launch_bounds__(256) qr_step_kernel(QrArgs a, int k, int iter)
   rmax = fmax(rho, block_max(rmax, scratch));
   const bool deficient = !(rho > 0.0) || rho < 1e-14 * rmax;
   for (int r = tid; r < nr; r += BT) a.Q[(long long)j * a.ldq + r0 + r] = deficient ? 0.0 : av[r] / rho;
-  if (b == 0) {
+  // Common case (a full-rank step, no column ever dropped): every block forms
+  // y^{(k)} itself (y^{(k-1)} is Yhist's previous column; the same operations
+  // in the same order in every block), so phase 5 needs no barrier; block 0
+  // alone writes R^{-1}, y, Yhist.  Otherwise block 0 does the rank-fallback
+  // work below and a grid barrier publishes the result.
+  const bool fast = !deficient && d0 == 0;  // uniform across the grid
+  double* ys = cv;
+  if (fast) {
+    ys = gv;
+    const double eta = (g / rho) / rho;
+    for (int i0 = warp * 4; i0 < j; i0 += nwarps * 4) {
+      double sr[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int l = i0 + lane; l < j; l += 32) {
+        const double cl = c1s[l] + cv[l];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (i0 + u < j && l >= i0 + u) sr[u] = fma(a.Rinv[(long long)(i0 + u) * a.kmax + l], cl, sr[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u;
+        const double sv = warp_sum(sr[u]);
+        if (lane == 0 && i < j) {
+          const double yi = a.Yhist[(long long)(j - 1) * a.kmax + i] - eta * sv;
+          ys[i] = yi;
+          if (b == 0) {
+            a.Rinv[(long long)i * a.kmax + j] = -sv / rho;
+            a.y[i] = yi;
+            a.Yhist[(long long)j * a.kmax + i] = yi;
+          }
+        }
+      }
+    }
+    if (tid == 0) {
+      ys[j] = eta;
+      if (b == 0) {
+        a.Rinv[(long long)j * a.kmax + j] = 1.0 / rho;
+        a.Rdiag[j] = rho;
+        a.y[j] = eta;
+        a.Yhist[(long long)j * a.kmax + j] = eta;
+        a.rankfb[j] = 0;
+      }
+    }
+    __syncthreads();
+  } else if (b == 0) {
     const double eta = deficient ? 0.0 : (g / rho) / rho;  // beta / rho, beta = q^T rhs = g / rho
     // w = Rinv[0:j, 0:j] (c1 + c2)
     // (R^{-1} is stored row-major: a warp reads row i contiguously)
@@ -322,12 +368,13 @@ __global__ void __launch_bounds__(256) qr_step_kernel(QrArgs a, int k, int iter)
     }
     if (tid == 0) a.rankfb[j] = d > 0 ? 1 : 0;
   }
-  grid.sync();
+  if (!fast) {
+    grid.sync();
+    for (int i = tid; i <= j; i += BT) ys[i] = __ldcg(&a.Yhist[(long long)j * a.kmax + i]);
+    __syncthreads();
+  }
 
   // phase 5: residual partials |Z y - sr0|^2 (top) and |F y|^2 (bottom)
-  double* ys = cv;
-  for (int i = tid; i <= j; i += BT) ys[i] = __ldcg(&a.Yhist[(long long)j * a.kmax + i]);
-  __syncthreads();
   const int ell = a.ell;
   const double *Zm = a.Z, *Fm = a.F;
   split_rows(nr, j + 1, ys, [&](int i, int r) {
@@ -350,8 +397,22 @@ __global__ void __launch_bounds__(256) qr_step_kernel(QrArgs a, int k, int iter)
     P5[(long long)b * pld + 0] = s_top;
     P5[(long long)b * pld + 1] = s_bot;
   }
-  grid.sync();
-  if (b == 0 && tid == 0) {
+  // the last block to arrive sums the partials in block order
+  bool reduce = false;
+  if (a.qdone) {
+    __shared__ bool last;
+    if (tid == 0) {
+      __threadfence();
+      last = atomicAdd(a.qdone, 1u) == (unsigned)NB - 1;
+    }
+    __syncthreads();
+    reduce = last && tid == 0;
+    if (reduce) __threadfence();
+  } else {
+    grid.sync();
+    reduce = b == 0 && tid == 0;
+  }
+  if (reduce) {
     double st = 0.0, sb = 0.0;
     for (int bb = 0; bb < NB; ++bb) {
       st += __ldcg(&P5[(long long)bb * pld + 0]);
@@ -359,6 +420,7 @@ __global__ void __launch_bounds__(256) qr_step_kernel(QrArgs a, int k, int iter)
     }
     a.sres[j] = sqrt(st);
     a.proj[j] = sqrt(st + a.lam * a.lam * sb);
+    if (a.qdone) *a.qdone = 0;
   }
 }
 
