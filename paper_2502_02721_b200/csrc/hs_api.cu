@@ -551,11 +551,14 @@ struct hs_op {
         // 0.157 -> 0.107 ms; its A^T, 8,192 shorter slices, stays at depth 1: 0.091 vs 0.106 ms)
         // between 32 and 96 slices per SM (config 3's A^T: 8,192 slices of 57 chunks) the
         // stream goes through the per-lane cp.async ring: 0.090 -> 0.080 ms (depth 1)
-        int depth = deep ? (M.nslices < 32LL * ctx->num_sms ? 2 : 8) : 0;
+        // (3: the full-occupancy kernel with unconditional, alternating-buffer prefetch;
+        // config 4 A 3.54 -> 3.47 ms, A^T 3.72 -> 3.64 ms against depth 0)
+        int depth = deep ? (M.nslices < 32LL * ctx->num_sms ? 2 : 8) : 3;
         if (const char* e = getenv("HS_D16_PIPE")) depth = atoi(e);
         auto pick = [&](auto p2c) {
           constexpr bool P2 = decltype(p2c)::value;
           return depth >= 4 ? sell_spmv_d16_kernel<V, Tin, T, P2, 4>
+               : depth == 3 ? sell_spmv_d16_kernel<V, Tin, T, P2, 3>
                : depth == 2 ? sell_spmv_d16_kernel<V, Tin, T, P2, 2>
                : depth == 1 ? sell_spmv_d16_kernel<V, Tin, T, P2, 1>
                             : sell_spmv_d16_kernel<V, Tin, T, P2, 0>;

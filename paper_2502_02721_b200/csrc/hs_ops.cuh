@@ -724,8 +724,34 @@ __device__ __forceinline__ T d16_row_pipe(const short* __restrict__ dp, const V*
   return acc;
 }
 
+// Variant of d16_row without the predicated prefetch: the next chunk's index is
+// clamped to the row's last chunk, so the (delta, value) loads are
+// unconditional and, with the loop unrolled twice, the two register buffers
+// alternate instead of being copied every chunk.  Same products and adds.
+template <int GM, class V, class Tin, class T>
+__device__ __forceinline__ T d16_row_u2(const short* __restrict__ dp, const V* __restrict__ vp, int c, int len,
+                                        const Tin* __restrict__ x, int m, int sh, int grid) {
+  T acc = T(0);
+  const int nq = (len + 3) >> 2, nfull = len >> 2;
+  if (nq == 0) return acc;
+  int2 d = __ldcs(reinterpret_cast<const int2*>(dp));
+  Chunk4<V> v = Chunk4<V>::load(vp);
+#pragma unroll 2
+  for (int q = 0; q < nfull; ++q) {
+    const long long qn = min(q + 1, nq - 1);
+    const int2 dn = __ldcs(reinterpret_cast<const int2*>(dp + qn * 128));
+    const Chunk4<V> vn = Chunk4<V>::load(vp + qn * 128);
+    d16_chunk<GM>(acc, c, d, v, x, m, sh, grid);
+    d = dn;
+    v = vn;
+  }
+  const int rem = len & 3;
+  if (rem) d16_tail<GM>(acc, c, d, v, rem, x, m, sh, grid);
+  return acc;
+}
+
 template <class V, class Tin, class T, bool POW2, int DEPTH = 0>
-__global__ void __launch_bounds__(256, DEPTH == 0 ? ((sizeof(T) == 4 && sizeof(V) == 4) ? 6 : 3)
+__global__ void __launch_bounds__(256, (DEPTH == 0 || DEPTH == 3) ? ((sizeof(T) == 4 && sizeof(V) == 4) ? 6 : 3)
                                        : DEPTH == 1 ? ((sizeof(T) == 4 && sizeof(V) == 4) ? 4 : 2)
                                        : DEPTH == 2 ? 2 : 1)
 sell_spmv_d16_kernel(long long rows, long long nslices, const long long* __restrict__ sptr,
@@ -751,7 +777,11 @@ sell_spmv_d16_kernel(long long rows, long long nslices, const long long* __restr
     const short* dp = dcol + base + lane * 4;
     const V* vp = val + base + lane * 4;
     T acc;
-    if constexpr (DEPTH >= 2) {
+    if constexpr (DEPTH == 3) {
+      if (!tr) acc = d16_row_u2<0, V, Tin, T>(dp, vp, c, len, xrow, 0, 0, grid);
+      else if (POW2) acc = d16_row_u2<1, V, Tin, T>(dp, vp, c, len, xT, grid - 1, gshift, grid);
+      else acc = d16_row_u2<2, V, Tin, T>(dp, vp, c, len, xT, 0, 0, grid);
+    } else if constexpr (DEPTH >= 2) {
       if (!tr) acc = d16_row_pipe<0, DEPTH, V, Tin, T>(dp, vp, c, len, xrow, 0, 0, grid);
       else if (POW2) acc = d16_row_pipe<1, DEPTH, V, Tin, T>(dp, vp, c, len, xT, grid - 1, gshift, grid);
       else acc = d16_row_pipe<2, DEPTH, V, Tin, T>(dp, vp, c, len, xT, 0, 0, grid);

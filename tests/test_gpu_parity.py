@@ -139,9 +139,9 @@ def test_tomography_builder_general_bins(hs, grid, angles, bins):
     "env",
     [{}, {"HS_C8": "1"}, {"HS_AT_C8": "1"}, {"HS_SINO_BLK": "0"}, {"HS_C8": "1", "HS_SINO_BLK": "2x16"},
      {"HS_D16_PIPE": "0"}, {"HS_D16_PIPE": "1"}, {"HS_D16_PIPE": "2"}, {"HS_D16_PIPE": "4"},
-     {"HS_D16_PIPE": "8"}],
+     {"HS_D16_PIPE": "8"}, {"HS_D16_PIPE": "3"}],
     ids=["default", "a_c8", "at_c8", "ray_order", "a_c8_blk2x16", "d16_depth0", "d16_depth1", "d16_depth2",
-         "d16_depth4", "d16_ring"],
+         "d16_depth4", "d16_ring", "d16_unrolled"],
 )
 def test_tomography_encodings_bitwise(hs, monkeypatch, grid, angles, bins, env):
     """Every device encoding of the tomography operator (8-bit transition codes
