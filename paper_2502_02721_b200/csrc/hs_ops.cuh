@@ -808,6 +808,230 @@ sell_spmv_d16_kernel(long long rows, long long nslices, const long long* __restr
   }
 }
 
+// ---- 16-bit deltas + dominant-value flags ("d16v") --------------------------------
+// A parallel-beam ray crosses most pixels of its path wall to wall, and every
+// such crossing has the same chord length, 1/max(|cos|, |sin|): about 41% of a
+// row's fp32 values are bitwise equal to the row's most frequent value.  The
+// d16v encoding keeps the 16-bit column deltas, steals their low bit as a flag
+// "value == the row's dominant value fv[slot]", and stores only the other
+// (explicit) values, compacted per slice chunk row in slot order (lane-major,
+// then entry).  A warp recovers each lane's offset into that stream with four
+// ballots.  The flag is set only on bitwise equality, so every product and
+// every add of the row sum is the one the d16 kernel makes: bit-identical.
+// Padding slots carry flag 1 (no explicit value) and delta 0.
+
+// fv per slot = mode of the row's first (up to) 32 values; explicit count and
+// the largest |delta| per slice
+template <class V>
+__global__ void sell_dominant_kernel(long long nslots, long long nslices, const long long* __restrict__ sptr,
+                                     const int* __restrict__ rlen, const short* __restrict__ dcol,
+                                     const V* __restrict__ val, V* __restrict__ fv, long long* __restrict__ nexp,
+                                     unsigned int* __restrict__ maxabs) {
+  const long long s = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (s >= nslices) return;
+  const int lane = threadIdx.x & 31;
+  const long long slot = s * 32 + lane;
+  const int len = slot < nslots ? rlen[slot] : 0;
+  const long long base = sptr[s];
+  auto at = [&](int e) { return base + (long long)(e >> 2) * 128 + lane * 4 + (e & 3); };
+  const int K = len < 32 ? len : 32;
+  V best = V(0);
+  int bestc = 0;
+  for (int i = 0; i < K; ++i) {
+    const V vi = val[at(i)];
+    int c = 0;
+    for (int j = 0; j < K; ++j) c += (val[at(j)] == vi && signbit(val[at(j)]) == signbit(vi)) ? 1 : 0;
+    if (c > bestc) { bestc = c; best = vi; }
+  }
+  if (slot < nslots) fv[slot] = best;
+  long long ne = 0;
+  unsigned int mx = 0;
+  for (int e = 0; e < len; ++e) {
+    const V v = val[at(e)];
+    ne += (v == best && signbit(v) == signbit(best)) ? 0 : 1;
+    const int d = dcol[at(e)];
+    const unsigned int a = (unsigned int)(d < 0 ? -d : d);
+    mx = a > mx ? a : mx;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ne += __shfl_xor_sync(0xffffffffu, ne, o);
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if (lane == 0) {
+    nexp[s] = ne;
+    atomicMax(maxabs, mx);
+  }
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// flag-shifted deltas in place; explicit values compacted to out[vptr[s] + ...]
+template <class V>
+__global__ void sell_d16v_fill_kernel(long long nslots, long long nslices, const long long* __restrict__ sptr,
+                                      const int* __restrict__ rlen, short* __restrict__ dcol, const V* __restrict__ val,
+                                      const V* __restrict__ fv, const long long* __restrict__ vptr, V* __restrict__ out) {
+  const long long s = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (s >= nslices) return;
+  const int lane = threadIdx.x & 31;
+  const long long slot = s * 32 + lane;
+  const int len = slot < nslots ? rlen[slot] : 0;
+  const V f = slot < nslots ? fv[slot] : V(0);
+  const long long base = sptr[s];
+  const int nq = (int)((sptr[s + 1] - base) >> 7);
+  const unsigned lt = lanemask_lt();
+  long long run = vptr[s];
+  for (int q = 0; q < nq; ++q) {
+    const long long p = base + (long long)q * 128 + lane * 4;
+    bool ex[4];
+    unsigned b[4];
+    int off = 0, tot = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e = q * 4 + i;
+      const V v = e < len ? val[p + i] : V(0);
+      ex[i] = e < len && !(v == f && signbit(v) == signbit(f));
+      b[i] = __ballot_sync(0xffffffffu, ex[i]);
+      off += __popc(b[i] & lt);
+      tot += __popc(b[i]);
+    }
+    int k = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e = q * 4 + i;
+      const int d = e < len ? (int)dcol[p + i] : 0;
+      dcol[p + i] = (short)((d << 1) | (ex[i] ? 0 : 1));
+      if (ex[i]) out[run + off + k++] = val[p + i];
+    }
+    run += tot;
+  }
+}
+
+// one chunk's flags -> explicit-value loads from the slice's compacted stream
+// (p = this lane's first explicit value of the chunk); flagged entries take fv
+__device__ __forceinline__ void d16v_vload(const int2 d, const float* __restrict__ p, float fv, float (&v)[4]) {
+  const bool e0 = !(d.x & 1), e1 = !((d.x >> 16) & 1), e2 = !(d.y & 1), e3 = !((d.y >> 16) & 1);
+  v[0] = e0 ? __ldcs(p) : fv;
+  p += e0;
+  v[1] = e1 ? __ldcs(p) : fv;
+  p += e1;
+  v[2] = e2 ? __ldcs(p) : fv;
+  p += e2;
+  v[3] = e3 ? __ldcs(p) : fv;
+}
+
+// offsets of this lane's explicit values within the chunk row, and the chunk row's total
+__device__ __forceinline__ void d16v_offsets(const int2 d, unsigned lt, int& off, int& tot) {
+  const unsigned b0 = __ballot_sync(0xffffffffu, !(d.x & 1));
+  const unsigned b1 = __ballot_sync(0xffffffffu, !((d.x >> 16) & 1));
+  const unsigned b2 = __ballot_sync(0xffffffffu, !(d.y & 1));
+  const unsigned b3 = __ballot_sync(0xffffffffu, !((d.y >> 16) & 1));
+  off = __popc(b0 & lt) + __popc(b1 & lt) + __popc(b2 & lt) + __popc(b3 & lt);
+  tot = __popc(b0) + __popc(b1) + __popc(b2) + __popc(b3);
+}
+
+template <int GM, class Tin, class T>
+__device__ __forceinline__ void d16v_chunk(T& acc, int& c, const int2 d, const float (&v)[4], int nv,
+                                           const Tin* __restrict__ x, int m, int sh, int grid) {
+  const int c0 = c + ((int)(short)(d.x & 0xffff) >> 1);
+  const int c1 = c0 + (d.x >> 17);
+  const int c2 = c1 + ((int)(short)(d.y & 0xffff) >> 1);
+  const int c3 = c2 + (d.y >> 17);
+  if (nv >= 4) {
+    const T x0 = gather_x<T>(x, gpos<GM>(c0, m, sh, grid));
+    const T x1 = gather_x<T>(x, gpos<GM>(c1, m, sh, grid));
+    const T x2 = gather_x<T>(x, gpos<GM>(c2, m, sh, grid));
+    const T x3 = gather_x<T>(x, gpos<GM>(c3, m, sh, grid));
+    acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v[0]), x0));
+    acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v[1]), x1));
+    acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v[2]), x2));
+    acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v[3]), x3));
+  } else if (nv > 0) {
+    acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v[0]), gather_x<T>(x, gpos<GM>(c0, m, sh, grid))));
+    if (nv > 1) acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v[1]), gather_x<T>(x, gpos<GM>(c1, m, sh, grid))));
+    if (nv > 2) acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v[2]), gather_x<T>(x, gpos<GM>(c2, m, sh, grid))));
+  }
+  c = c3;
+}
+
+// The warp walks every chunk row of its slice (the ballots need all lanes);
+// deltas run two chunks ahead, explicit values one chunk ahead.
+template <int GM, class Tin, class T>
+__device__ __forceinline__ T d16v_slice_row(const short* __restrict__ dp, const float* __restrict__ vs, float fv,
+                                            int c, int len, int nqs, const Tin* __restrict__ x, int m, int sh,
+                                            int grid) {
+  T acc = T(0);
+  if (nqs == 0) return acc;
+  const unsigned lt = lanemask_lt();
+  int2 d = __ldcs(reinterpret_cast<const int2*>(dp));
+  int2 dn = __ldcs(reinterpret_cast<const int2*>(dp + (long long)min(1, nqs - 1) * 128));
+  int off, tot;
+  d16v_offsets(d, lt, off, tot);
+  float v[4];
+  d16v_vload(d, vs + off, fv, v);
+  vs += tot;
+#pragma unroll 1
+  for (int q = 0; q < nqs; ++q) {
+    const int2 dnn = __ldcs(reinterpret_cast<const int2*>(dp + (long long)min(q + 2, nqs - 1) * 128));
+    d16v_offsets(dn, lt, off, tot);
+    float vn[4];
+    d16v_vload(dn, vs + off, fv, vn);  // past the last chunk: dn repeats it, the loads re-read it
+    vs += (q + 1 < nqs) ? tot : 0;
+    d16v_chunk<GM, Tin, T>(acc, c, d, v, len - 4 * q, x, m, sh, grid);
+    d = dn;
+    dn = dnn;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = vn[i];
+  }
+  return acc;
+}
+
+template <class Tin, class T, bool POW2>
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 5 : 3)
+sell_spmv_d16v_kernel(long long rows, long long nslices, const long long* __restrict__ sptr,
+                      const long long* __restrict__ vptr, const int* __restrict__ rlen, const int* __restrict__ rbase,
+                      const short* __restrict__ dcol, const float* __restrict__ val, const float* __restrict__ fv,
+                      const Tin* __restrict__ xrow, const Tin* __restrict__ xT, const unsigned char* __restrict__ sflag,
+                      int grid, int gshift, const int* __restrict__ rperm, const int* __restrict__ sorder,
+                      unsigned int* __restrict__ sched, T* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    unsigned int i = 0;
+    if (lane == 0) i = atomicAdd(&sched[0], 1u);
+    i = __shfl_sync(0xffffffffu, i, 0);
+    if (i >= nslices) break;
+    const long long s = sorder ? (long long)sorder[i] : (long long)i;
+    const bool tr = sflag != nullptr && sflag[s];
+    const long long slot = s * 32 + lane;
+    const long long row = rperm ? (long long)rperm[slot] : slot;
+    const int len = rlen[slot];
+    const int c = rbase[slot];
+    const float f = fv[slot];
+    const long long base = sptr[s];
+    const int nqs = (int)((sptr[s + 1] - base) >> 7);
+    const short* dp = dcol + base + lane * 4;
+    const float* vs = val + vptr[s];
+    T acc;
+    if (!tr) acc = d16v_slice_row<0, Tin, T>(dp, vs, f, c, len, nqs, xrow, 0, 0, grid);
+    else if (POW2) acc = d16v_slice_row<1, Tin, T>(dp, vs, f, c, len, nqs, xT, grid - 1, gshift, grid);
+    else acc = d16v_slice_row<2, Tin, T>(dp, vs, f, c, len, nqs, xT, 0, 0, grid);
+    if (row >= 0 && row < rows) y[row] = acc;
+  }
+  if (lane == 0) {
+    __threadfence();
+    const unsigned int done = atomicAdd(&sched[1], 1u);
+    if (done == gridDim.x * (blockDim.x >> 5) - 1) {
+      sched[0] = 0;
+      sched[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
 // ---- 8-bit transition codes (tomography operators) ---------------------------------
 // The columns of a tomography row are points (r, c) of a 2D index space that
 // a ray (or, for A^T, a pixel's sequence of rays) walks through in small steps:
