@@ -363,8 +363,8 @@ static bool sell_try_delta16(hs_ctx* ctx, Sell& S) {
 // Opt-in (HS_D16V=1): config 4's A stream shrinks from 6 to 4.3 B/nonzero
 // (59% of values explicit), bit-identical, but the kernel measured 4.41 ms
 // against d16's 3.47 -- the per-lane variable-rate value loads (four scalar
-// loads and four ballots per chunk) move the limit from HBM to the L1/LSU
-// pipe, which the gathers already hold at ~80%.
+// loads and four ballots per chunk) raise the kernel from 44 to 111 warp
+// instructions per chunk, moving the limit from HBM to issue.
 template <class V>
 static bool sell_try_dominant(hs_ctx* ctx, Sell& S) {
   if constexpr (sizeof(V) != 4) {
