@@ -688,11 +688,12 @@ struct hs_op {
         dense_seq_gemv_kernel<V, Tin, T><<<grid_for(rows, 256, 1 << 30), 256, 1024 * sizeof(T), s>>>(rows, cols, Mcm,
                                                                                                      xi, yo);
       } else {
-        const size_t smem = dense_tile_smem(sizeof(T));
-        if (smem > 48 * 1024)
-          CK(cudaFuncSetAttribute(dense_tile_gemv_kernel<V, Tin, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
-        dense_tile_gemv_kernel<V, Tin, T><<<(int)((rows + 31) / 32), 256, smem, s>>>(rows, cols, Mcm, xi, yo);
+        const bool rb32 = env_flag("HS_DENSE_RB32");
+        const int RB = rb32 ? 32 : 8;
+        const size_t smem = rb32 ? dense_tile_smem(sizeof(T), 32, 256) : dense_tile_smem(sizeof(T), 8, 1024);
+        auto kern = rb32 ? dense_tile_gemv_kernel<V, Tin, T, 32, 256> : dense_tile_gemv_kernel<V, Tin, T, 8, 1024>;
+        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<(int)((rows + RB - 1) / RB), 256, smem, s>>>(rows, cols, Mcm, xi, yo);
       }
       CKL();
     } else if (kind == OP_PSF && sharded) {

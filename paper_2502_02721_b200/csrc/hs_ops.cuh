@@ -111,17 +111,20 @@ dense_seq_gemv_kernel(long long rows, long long cols, const V* __restrict__ Acm,
   if (r < rows) y[r] = acc;
 }
 
-// Tiled variant (the default): a block owns 32 rows; for each tile of 256
-// columns all 256 threads form the 32 x 256 products (rounded, independent,
-// many loads in flight) into shared memory, then warp 0 adds each row's
+// Tiled variant (the default): a block owns RB rows; for each tile of CT
+// columns all 256 threads form the RB x CT products (rounded, independent,
+// many loads in flight) into shared memory, then RB threads add each row's
 // products left to right.  Same operation sequence per row as the simple
 // kernel -- product rounded, then added, columns ascending -- so bit-identical;
 // the serial part is a shared-memory add chain instead of a global-load chain.
-template <class V, class Tin, class T>
+// Default RB = 8, CT = 1024: config 1 (1024 x 1024) runs as 128 blocks, one
+// barrier-separated product phase and one 1024-long add chain per row
+// (RB = 32, CT = 256 -- 32 blocks, four phases -- is HS_DENSE_RB32=1).
+template <class V, class Tin, class T, int RB = 8, int CT = 1024>
 __global__ void __launch_bounds__(256)
 dense_tile_gemv_kernel(long long rows, long long cols, const V* __restrict__ Acm, const Tin* __restrict__ x,
                        T* __restrict__ y) {
-  constexpr int RB = 32, CT = 256, LD = CT + 1;
+  constexpr int LD = CT + 2;  // even: 16-byte rows for the paired chain reads, 8 rows on distinct banks
   extern __shared__ __align__(16) unsigned char dense_smem[];
   T* prod = reinterpret_cast<T*>(dense_smem);  // RB x LD
   T* xs = prod + RB * LD;                      // CT
@@ -132,6 +135,7 @@ dense_tile_gemv_kernel(long long rows, long long cols, const V* __restrict__ Acm
     const int cn = (int)min((long long)CT, cols - c0);
     for (int i = tid; i < cn; i += blockDim.x) xs[i] = cvt<T>(x[c0 + i]);
     __syncthreads();
+#pragma unroll 8
     for (int idx = tid; idx < RB * cn; idx += blockDim.x) {
       const int rr = idx % RB, cc = idx / RB;
       const long long r = r0 + rr;
@@ -140,15 +144,25 @@ dense_tile_gemv_kernel(long long rows, long long cols, const V* __restrict__ Acm
     __syncthreads();
     if (tid < RB) {
       const T* pr = prod + tid * LD;
+      int j = 0;
+      if constexpr (sizeof(T) == 8) {  // two products per shared-memory load; same adds, same order
+        const double2* p2 = reinterpret_cast<const double2*>(pr);
 #pragma unroll 8
-      for (int j = 0; j < cn; ++j) acc = Rn<T>::add(acc, pr[j]);
+        for (; j + 1 < cn; j += 2) {
+          const double2 t = p2[j >> 1];
+          acc = Rn<T>::add(acc, t.x);
+          acc = Rn<T>::add(acc, t.y);
+        }
+      }
+#pragma unroll 8
+      for (; j < cn; ++j) acc = Rn<T>::add(acc, pr[j]);
     }
     __syncthreads();
   }
   if (tid < RB && r0 + tid < rows) y[r0 + tid] = acc;
 }
 
-inline size_t dense_tile_smem(size_t tsize) { return (32 * 257 + 256) * tsize; }
+inline size_t dense_tile_smem(size_t tsize, int rb, int ct) { return ((size_t)rb * (ct + 2) + ct) * tsize; }
 
 // --------------------------------------------------------------------------
 // PSF stencil: zero-boundary 'same' convolution (transpose = 0) or correlation
