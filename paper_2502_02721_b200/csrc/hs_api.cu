@@ -11,6 +11,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
@@ -64,7 +65,7 @@ struct HsError {
                                 cudaGetErrorString(e_));                               \
   } while (0)
 
-static unsigned long long g_launches = 0;  // kernels launched by this library (all streams)
+static std::atomic<unsigned long long> g_launches{0};  // kernels launched by this library (all streams)
 #define CKL()                   \
   do {                          \
     CK(cudaGetLastError());     \
@@ -88,34 +89,48 @@ int guarded(F&& f) {
 size_t dsize(int dt) { return dt == HS_F64 ? 8 : (dt == HS_F32 ? 4 : 2); }
 long long round_up(long long a, long long b) { return (a + b - 1) / b * b; }
 
-// Stream-ordered allocations on the context stream of each device, from a
-// memory pool that keeps freed blocks (repeated solves reuse the 7.5 GB of
-// bases instead of paying cudaMalloc/cudaFree and page unmapping each time).
-static cudaStream_t g_dev_stream[64] = {};
-
-static cudaStream_t alloc_stream() {
-  int d = 0;
-  cudaGetDevice(&d);
-  return (d >= 0 && d < 64) ? g_dev_stream[d] : nullptr;
-}
+// Stream-ordered allocations.  Every buffer is allocated and freed on the
+// main stream of the context active on the calling thread (CtxScope, set by
+// each C entry point), from a memory pool that keeps freed blocks (repeated
+// solves reuse the 7.5 GB of bases instead of paying cudaMalloc/cudaFree and
+// page unmapping each time).  The stream is reference-counted: a context's
+// operators, sketches and results keep it alive after hs_ctx_destroy, so a
+// late free is still ordered after the work that used the buffer.  Without
+// an active context (none of the entry points) the synchronous allocator is
+// used.
+struct StreamRef {
+  cudaStream_t s = nullptr;
+  int device = 0;
+  ~StreamRef() {
+    if (!s) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(device);
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    cudaSetDevice(cur);
+  }
+};
+static thread_local std::shared_ptr<StreamRef> tl_alloc;
 
 // device buffer with RAII
 struct DBuf {
   void* p = nullptr;
   size_t bytes = 0;
-  cudaStream_t st = nullptr;
+  std::shared_ptr<StreamRef> owner;
   DBuf() = default;
   explicit DBuf(size_t b, bool zero = true) { alloc(b, zero); }
   void alloc(size_t b, bool zero = true) {
     release();
     bytes = b;
     if (b) {
-      st = alloc_stream();
-      if (st) {
-        CK(cudaMallocAsync(&p, b, st));
-        if (zero) CK(cudaMemsetAsync(p, 0, b, st));
-        // buffers are also touched by synchronous copies on the legacy stream
-        CK(cudaStreamSynchronize(st));
+      owner = tl_alloc;
+      if (owner) {
+        CK(cudaMallocAsync(&p, b, owner->s));
+        if (zero) CK(cudaMemsetAsync(p, 0, b, owner->s));
+        // buffers are also filled by pageable-host copies and read by the
+        // context's second stream: make the allocation complete now
+        CK(cudaStreamSynchronize(owner->s));
       } else {
         CK(cudaMalloc(&p, b));
         if (zero) CK(cudaMemset(p, 0, b));
@@ -124,22 +139,33 @@ struct DBuf {
   }
   void release() {
     if (p) {
-      if (st) cudaFreeAsync(p, st);
+      if (owner) cudaFreeAsync(p, owner->s);  // ordered after the owning stream's work
       else cudaFree(p);
     }
     p = nullptr;
     bytes = 0;
+    owner.reset();
   }
   ~DBuf() { release(); }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes), st(o.st) { o.p = nullptr; o.bytes = 0; }
+  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes), owner(std::move(o.owner)) { o.p = nullptr; o.bytes = 0; }
   DBuf& operator=(DBuf&& o) noexcept {
     release();
-    p = o.p; bytes = o.bytes; st = o.st; o.p = nullptr; o.bytes = 0;
+    p = o.p; bytes = o.bytes; owner = std::move(o.owner); o.p = nullptr; o.bytes = 0;
     return *this;
   }
   template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+// the context whose main stream owns allocations made on this thread (DBuf)
+struct CtxScope {
+  std::shared_ptr<StreamRef> prev;
+  template <class C>
+  explicit CtxScope(const C* c) : prev(tl_alloc) {
+    if (c) tl_alloc = c->main;
+  }
+  ~CtxScope() { tl_alloc = prev; }
 };
 
 // experiment switches (tools/ab_spmv.py): set and not "0"/empty
@@ -168,7 +194,8 @@ struct KStat {
 
 struct hs_ctx {
   int device = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;  // == main->s
+  std::shared_ptr<StreamRef> main;
   cudaStream_t aux = nullptr;  // second stream: sketches + projected solve overlap the basis passes
   int num_sms = 148;
   int nranks = 1, rank = 0;
@@ -234,7 +261,9 @@ struct hs_ctx {
   }
   void harvest() {
     if (pending.empty()) return;
+    // pairs recorded on either stream (aux: sketches, projected solves)
     CK(cudaStreamSynchronize(stream));
+    CK(cudaStreamSynchronize(aux));
     for (auto& p : pending) {
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, p.a, p.b));
@@ -256,11 +285,7 @@ struct L2Window {
   L2Window(cudaStream_t st, const void* p, size_t bytes) {
     const bool on = env_flag("HS_L2PERSIST");
     if (!on || p == nullptr) return;
-    static bool limit_set = false;
-    if (!limit_set) {
-      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)64 << 20);
-      limit_set = true;
-    }
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)64 << 20);  // per device, idempotent
     cudaStreamAttrValue a = {};
     a.accessPolicyWindow.base_ptr = const_cast<void*>(p);
     a.accessPolicyWindow.num_bytes = bytes;
@@ -589,7 +614,7 @@ struct hs_op {
         constexpr int MINB = (sizeof(T) == 4 && sizeof(V) == 4) ? 6 : 3;
         auto kern = M.c8g.mode == 0 ? sell_spmv_c8_kernel<V, Tin, T, 0, 3, MINB> : sell_spmv_c8_kernel<V, Tin, T, 1, 3, MINB>;
         const int smem = C8Lane<V, 3>::smem_bytes(256);
-        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        CK(ensure_smem((const void*)kern, smem));
         kern<<<grid, 256, smem, s>>>(M.rows, M.nslices, M.sptr.as<long long>(), M.rlen.as<int>(), M.rbase.as<int>(),
                                   M.code.as<unsigned char>(), M.xoff.as<int>(), M.exc.as<int>(), M.val.as<V>(), xi,
                                   tflag ? xT.as<Tin>() : nullptr, tflag ? sflag.as<unsigned char>() : nullptr, M.c8g.G,
@@ -645,7 +670,7 @@ struct hs_op {
           auto rk = p2 ? sell_spmv_d16_ring_kernel<V, Tin, T, true, NS, MINB>
                        : sell_spmv_d16_ring_kernel<V, Tin, T, false, NS, MINB>;
           const int smem = D16Ring<V, NS>::smem_bytes(256);
-          if (smem > 48 * 1024) CK(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+          CK(ensure_smem((const void*)rk, smem));
           rk<<<grid, 256, smem, s>>>(M.rows, M.nslices, M.sptr.as<long long>(), M.rlen.as<int>(), M.rbase.as<int>(),
                                      M.dcol.as<short>(), M.val.as<V>(), xi, tflag ? xT.as<Tin>() : nullptr,
                                      tflag ? sflag.as<unsigned char>() : nullptr, img_grid, gshift >= 0 ? gshift : 0,
@@ -692,7 +717,7 @@ struct hs_op {
         const int RB = rb32 ? 32 : 8;
         const size_t smem = rb32 ? dense_tile_smem(sizeof(T), 32, 256) : dense_tile_smem(sizeof(T), 8, 1024);
         auto kern = rb32 ? dense_tile_gemv_kernel<V, Tin, T, 32, 256> : dense_tile_gemv_kernel<V, Tin, T, 8, 1024>;
-        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(ensure_smem((const void*)kern, smem));
         kern<<<(int)((rows + RB - 1) / RB), 256, smem, s>>>(rows, cols, Mcm, xi, yo);
       }
       CKL();
@@ -731,7 +756,7 @@ struct hs_op {
         const size_t smem = G::smem(kh);
         auto kern = transpose ? psf_stencil_rb_kernel<V, Tin, T, KWc, G::R, G::TXT, G::TY, true>
                               : psf_stencil_rb_kernel<V, Tin, T, KWc, G::R, G::TXT, G::TY, false>;
-        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(ensure_smem((const void*)kern, smem));
         kern<<<grid, G::TXT * G::TY, smem, s>>>(rows, W, kh, K.as<V>(), xi, yo, out_row0, out_rows);
         CKL();
       };
@@ -1145,7 +1170,7 @@ struct Solver {
     if (ps > 0) {
       const int nslots = square ? K + 1 : 2 * K + 2;
       posd.alloc((size_t)nslots * ps * sizeof(long long), false);
-      CK(cudaMemcpy(posd.p, cfg.pivot_positions, (size_t)nslots * ps * sizeof(long long), cudaMemcpyHostToDevice));
+      CK(cudaMemcpyAsync(posd.p, cfg.pivot_positions, (size_t)nslots * ps * sizeof(long long), cudaMemcpyHostToDevice, s));
       const long long dt = square ? n : m;
       for (DBuf* b : {&permT, &whereT}) {
         b->alloc(dt * sizeof(long long), false);
@@ -1311,7 +1336,7 @@ struct Solver {
       if (lamon) {
         std::vector<double> eye((size_t)ell * (K + 1), 0.0);
         for (int j = 0; j <= K && j < ell; ++j) eye[(size_t)j * ell + j] = 1.0;
-        CK(cudaMemcpy(Fb.p, eye.data(), eye.size() * sizeof(double), cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(Fb.p, eye.data(), eye.size() * sizeof(double), cudaMemcpyHostToDevice, s));
       }
       CK(cudaStreamSynchronize(s));
     }
@@ -1367,7 +1392,7 @@ struct Solver {
       Prof p(ctx, side == 0 && !square ? "elim_D" : "elim_L", bytes);
       auto kern = v1 ? (kx ? elim_pass_kernel<T, B, 1, true> : elim_pass_kernel<T, B, 1, false>)
                      : (kx ? elim_pass_kernel<T, B, VEC, true> : elim_pass_kernel<T, B, VEC, false>);
-      if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      CK(ensure_smem((const void*)kern, smem));
       (void)ldv;
       kern<<<g, 256, smem, s>>>(
           len, 0, basis, square || side == 1 ? ldn : ldm, nullptr, k, cvec.as<T>(), vec, kx, yx, nullptr,
@@ -1803,15 +1828,17 @@ int hs_ctx_create(int device, hs_ctx** out) {
     int prio_lo = 0, prio_hi = 0;
     CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     if (env_flag("HS_FLAT_PRIO")) prio_lo = prio_hi = 0;
-    CK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi));
+    c->main = std::make_shared<StreamRef>();
+    c->main->device = device;
+    CK(cudaStreamCreateWithPriority(&c->main->s, cudaStreamNonBlocking, prio_hi));
+    c->stream = c->main->s;
     CK(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, prio_lo));
-    if (device < 64 && !g_dev_stream[device]) {
+    {
       // keep freed blocks in the device pool (no release back to the driver)
       cudaMemPool_t pool;
       CK(cudaDeviceGetDefaultMemPool(&pool, device));
       unsigned long long thr = ~0ULL;
       CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-      g_dev_stream[device] = c->stream;
     }
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     *out = c;
@@ -1830,10 +1857,11 @@ int hs_ctx_destroy(hs_ctx* ctx) {
     for (auto e : ctx->pool_timed) cudaEventDestroy(e);
     for (auto e : ctx->pool_sync) cudaEventDestroy(e);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
-    if (ctx->device < 64 && g_dev_stream[ctx->device] == ctx->stream) g_dev_stream[ctx->device] = nullptr;
     cudaStreamSynchronize(ctx->aux);
     cudaStreamDestroy(ctx->aux);
-    cudaStreamDestroy(ctx->stream);
+    // the main stream lives on while operators / sketches / results of this
+    // context still hold buffers allocated on it (StreamRef)
+    ctx->main.reset();
     delete ctx;
   });
 }

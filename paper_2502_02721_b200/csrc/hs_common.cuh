@@ -12,7 +12,31 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 namespace hs {
+
+// Raise a kernel's dynamic shared-memory limit on the current device, once
+// per (kernel, device) and thread-safely: the attribute is per device, so a
+// process with contexts on several GPUs (or concurrent solves) must not share
+// a single "already raised" flag.
+inline cudaError_t ensure_smem(const void* kern, size_t bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> raised;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(mu);
+  const auto key = std::make_pair(kern, dev);
+  auto it = raised.find(key);
+  if (it != raised.end() && it->second >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) raised[key] = bytes;
+  return e;
+}
 
 constexpr int kWarp = 32;
 

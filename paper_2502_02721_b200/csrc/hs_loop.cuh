@@ -208,11 +208,7 @@ inline void launch_fsub(cudaStream_t s, const T* u, const long long* pos, const 
     return e && *e && *e != '0';
   }();
   if (smem <= 200 * 1024 && !legacy) {
-    static size_t attr = 48 * 1024;  // per instantiation
-    if (smem > attr) {
-      cudaFuncSetAttribute(fsub_panel_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr = 200 * 1024;
-    }
+    if (smem > 48 * 1024) ensure_smem((const void*)fsub_panel_kernel<T>, 200 * 1024);
     fsub_panel_kernel<T><<<1, 256, smem, s>>>(u, pos, 0, P, ldp, k, st, iter, side, c, hcol);
   } else if (k <= 64) {
     fsub_warp_kernel<T, 2><<<1, 32, 0, s>>>(u, pos, 0, P, ldp, nullptr, k, st, iter, side, c, hcol);

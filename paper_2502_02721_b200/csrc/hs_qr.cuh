@@ -439,7 +439,7 @@ inline cudaError_t launch_qr_step(const QrArgs& qa, int k, int iter, int NB, siz
 // kernel attributes for a step with `smem` bytes of dynamic shared memory
 inline cudaError_t prepare_qr_step(size_t smem) {
   if (smem <= 48 * 1024) return cudaSuccess;
-  return cudaFuncSetAttribute(qr_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  return ensure_smem((const void*)qr_step_kernel, smem);
 }
 
 }  // namespace hs

@@ -132,12 +132,7 @@ template <class Tin, int NV, int UNR = 2>
 inline void gauss_partial_launch(dim3 grid, cudaStream_t s, int ell, long long m, long long col_offset,
                                  long long tile_cols, uint2 key, const Tin* v, long long ldv, int nv, double* part) {
   const size_t smem = (size_t)GAUSS_CH * NV * sizeof(double);
-  static bool attr = false;  // per instantiation
-  if (!attr && smem > 48 * 1024) {
-    cudaFuncSetAttribute(sketch_gauss_partial_kernel<Tin, NV, UNR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    attr = true;
-  }
+  ensure_smem((const void*)sketch_gauss_partial_kernel<Tin, NV, UNR>, smem);
   sketch_gauss_partial_kernel<Tin, NV, UNR><<<grid, 256, smem, s>>>(ell, m, col_offset, tile_cols, key, v, ldv, nv,
                                                                     part);
 }
