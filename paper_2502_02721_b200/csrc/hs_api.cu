@@ -11,6 +11,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -548,6 +549,8 @@ struct hs_op {
   // padded block sizes m_blk / n_blk (the all-gathered vectors are P*blk long)
   bool sharded = false;
   long long m_off = 0, m_loc = 0, m_blk = 0, n_off = 0, n_loc = 0, n_blk = 0;
+  // tomography (hs_op_tomo_create): image side
+  long long tomo_grid = 0;
   // tomography: per-slice transposed-layout flags of As and the scratch copy of x
   int img_grid = 0;
   DBuf sflag;
@@ -821,6 +824,17 @@ struct hs_op {
     }
   }
 
+  // Shard granule of the range (side 0, length m) / domain (side 1, length
+  // n) vectors: row shards are whole granules (rays in power-of-two blocks;
+  // 8 image rows), and the sketches of these vectors sum their partials
+  // granule by granule (hs_sketch.cuh), so solves give the same bits for any
+  // number of ranks.  Operators that never shard: one granule.
+  long long granule(int side) const {
+    if (kind == OP_CSR && tomo_grid > 0) return side == 0 ? std::max<long long>(64, shard_granule(m)) : 8LL * tomo_grid;
+    if (kind == OP_PSF) return 8LL * W;
+    return side == 0 ? m : n;
+  }
+
   long long nnz_total() const { return kind == OP_CSR ? A.nnz : (kind == OP_DENSE ? m * n : 0); }
 };
 
@@ -913,64 +927,221 @@ struct hs_sketch {
   unsigned long long seed = 0;
   int zeta = 0;
   DBuf S;                 // dense row-major fp64
-  DBuf rowptr, scol;      // sparse sign, by sketch row (also CSR kind: cols)
+  DBuf rowptr, scol;      // CSR kind: rows, cols
   DBuf cval;              // CSR kind: fp64 values
-  DBuf part;              // gaussian tile partials
-  long long tile_cols = 0;
-  int ntiles = 0;
+  long long tile = 0;     // columns per partial tile (power of two; sparse sign: at most)
+  // sparse sign: the tile layouts (hs_sketch.cuh: sketch_sparse_gather_kernel),
+  // one per tile size in use, built on first use from the regenerated entries
+  struct SparseLayout {
+    long long tc = 0, ntiles = 0, nent = 0;
+    int nsl = 0;
+    DBuf tbase, soff, perm, ent;
+  };
+  mutable std::map<long long, std::unique_ptr<SparseLayout>> layouts;
+  mutable std::mutex lay_mu;
+  const SparseLayout& sparse_layout(long long tc) const;
+  // tile size used with granule G: sparse-sign tiles must divide G
+  long long tile_for(long long G) const {
+    if (kind != HS_SKETCH_SPARSE_SIGN || G >= m) return tile;  // one granule: no alignment needed
+    const long long low = G & -G;
+    return std::min(tile, low);
+  }
   uint2 key() const { return make_uint2((unsigned)seed, (unsigned)(seed >> 32)); }
+  bool tiled() const { return kind != HS_SKETCH_CSR; }
+  double scale() const {
+    return kind == HS_SKETCH_GAUSSIAN ? 1.0 / std::sqrt((double)ell)
+         : kind == HS_SKETCH_SPARSE_SIGN ? 1.0 / std::sqrt((double)zeta) : 1.0;
+  }
+  int tpg(long long G) const { return (int)((G + tile_for(G) - 1) / tile_for(G)); }
+  // partial slots for `cols` input entries cut in granules of G
+  long long slots(long long cols, long long G) const { return tiled() ? ((cols + G - 1) / G) * tpg(G) : 0; }
+  // scratch (doubles) for the partials of nv vectors over `cols` input entries
+  long long scratch_elems(int nv, long long cols, long long G) const { return (long long)nv * slots(cols, G) * ell; }
 
+  // partials of nv vectors (column stride ldv) over the local entries
+  // [0, loc) = global input entries [off, off + loc), off a multiple of the
+  // granule G: part[(w * tstride + slot) * ell + i]
   template <class Tin>
-  void apply_t(const void* v, double* z, cudaStream_t st) const {
-    cudaStream_t s = st ? st : ctx->stream;
-    const Tin* vi = reinterpret_cast<const Tin*>(v);
-    if (kind == HS_SKETCH_DENSE) {
-      Prof p(ctx, "sketch_dense", (double)ell * m * 8, s);
-      sketch_dense_kernel<double, Tin><<<(int)ell, 256, 0, s>>>((int)ell, m, S.as<double>(), m, vi, z);
-      CKL();
-    } else if (kind == HS_SKETCH_GAUSSIAN) {
-      apply_many_t<Tin>(v, 0, 1, z, 0, st);
-    } else if (kind == 3) {
-      Prof p(ctx, "sketch_csr", 0.0, s);
-      sketch_csr_kernel<Tin><<<(int)ell, 256, 0, s>>>((int)ell, rowptr.as<long long>(), scol.as<int>(),
-                                                      cval.as<double>(), vi, z);
-      CKL();
-    } else {
-      Prof p(ctx, "sketch_sparse", (double)m * zeta * 4 + (double)m * sizeof(Tin), s);
-      sketch_sparse_kernel<Tin><<<(int)ell, 256, 0, s>>>((int)ell, rowptr.as<long long>(), scol.as<int>(), 0, m, vi,
-                                                         1.0 / std::sqrt((double)zeta), z);
-      CKL();
-    }
-  }
-  // z[:, w] = S v_w for nv vectors with column stride ldv (z column stride ldz).
-  // The Gaussian kind generates S once for the whole batch (hs_sketch.cuh);
-  // the other kinds apply column by column.  Results equal nv single applies.
-  template <class Tin>
-  void apply_many_t(const void* v, long long ldv, int nv, double* z, long long ldz, cudaStream_t st) const {
-    cudaStream_t s = st ? st : ctx->stream;
-    const Tin* vi = reinterpret_cast<const Tin*>(v);
+  void partials_t(const Tin* v, long long ldv, int nv, long long off, long long loc, long long G, double* part,
+                  long long tstride, cudaStream_t s) const {
+    if (off % G != 0) fail(HS_ERR_VALUE, "sketch block offset %lld is not a multiple of the granule (%lld)", off, G);
+    const TileMap tm{G, tile_for(G), loc, tpg(G)};
     if (kind == HS_SKETCH_GAUSSIAN) {
-      Prof p(ctx, "sketch_gauss", (double)nv * m * sizeof(Tin), s);
       CK(cudaGetLastError());
-      g_launches += gauss_sketch_launch<Tin>(s, (int)ell, m, 0, tile_cols, key(), vi, ldv, nv, part.as<double>(), z,
-                                             ldz);
+      g_launches += gauss_partials<Tin>(s, (int)ell, tm, off, key(), v, ldv, nv, part, tstride);
       CK(cudaGetLastError());
-    } else {
-      for (int w = 0; w < nv; ++w) apply_t<Tin>(vi + (long long)w * ldv, z + (long long)w * ldz, st);
+      return;
+    }
+    const long long nt = tm.slots();
+    for (int w = 0; w < nv; ++w) {
+      const Tin* vw = v + (long long)w * ldv;
+      double* pw = part + (long long)w * tstride * ell;
+      if (nt == 0) continue;
+      if (kind == HS_SKETCH_DENSE) {
+        sketch_dense_tile_kernel<Tin><<<dim3((unsigned)nt, (unsigned)((ell + 7) / 8)), 256, 0, s>>>((int)ell, tm, off,
+                                                                                                  S.as<double>(), m, vw,
+                                                                                                  pw);
+        CKL();
+      } else if (kind == HS_SKETCH_SPARSE_SIGN) {
+        const SparseLayout& L = sparse_layout(tm.tc);
+        sparse_partials<Tin>(s, (int)ell, tm, off, L.tbase.as<long long>(), L.soff.as<int>(),
+                             L.perm.as<unsigned short>(), L.ent.as<unsigned short>(), vw, pw);
+        CKL();
+      } else {
+        fail(HS_ERR_NOTIMPL, "explicit CSR sketches have no tile partials");
+      }
     }
   }
-  void apply_many(const void* v, int vdt, long long ldv, int nv, double* z, long long ldz,
-                  cudaStream_t st = nullptr) const {
-    if (vdt == HS_F64) apply_many_t<double>(v, ldv, nv, z, ldz, st);
-    else if (vdt == HS_F32) apply_many_t<float>(v, ldv, nv, z, ldz, st);
-    else apply_many_t<__nv_bfloat16>(v, ldv, nv, z, ldz, st);
+  void partials(const void* v, int vdt, long long ldv, int nv, long long off, long long loc, long long G, double* part,
+                long long tstride, cudaStream_t s) const {
+    if (vdt == HS_F64) partials_t<double>(reinterpret_cast<const double*>(v), ldv, nv, off, loc, G, part, tstride, s);
+    else if (vdt == HS_F32) partials_t<float>(reinterpret_cast<const float*>(v), ldv, nv, off, loc, G, part, tstride, s);
+    else partials_t<__nv_bfloat16>(reinterpret_cast<const __nv_bfloat16*>(v), ldv, nv, off, loc, G, part, tstride, s);
   }
-  void apply(const void* v, int vdt, double* z, cudaStream_t st = nullptr) const {
-    if (vdt == HS_F64) apply_t<double>(v, z, st);
-    else if (vdt == HS_F32) apply_t<float>(v, z, st);
-    else apply_t<__nv_bfloat16>(v, z, st);
+  // z[w * ldz + i] = scale * the ordered sum of all partials of the m inputs,
+  // laid out as blocks of gpr granules ([block][w][slot][i])
+  void reduce(const double* part, int nv, long long G, long long gpr, double* z, long long ldz, cudaStream_t s) const {
+    sketch_tile_reduce_kernel<<<dim3((unsigned)((ell + RROWS - 1) / RROWS), nv), RROWS * RPH, 0, s>>>(
+        (int)ell, m, G, tile_for(G), tpg(G), gpr, nv, part, scale(), z, ldz);
+    CKL();
+  }
+  const char* prof_name() const {
+    return kind == HS_SKETCH_GAUSSIAN ? "sketch_gauss" : kind == HS_SKETCH_SPARSE_SIGN ? "sketch_sparse"
+         : kind == HS_SKETCH_DENSE ? "sketch_dense" : "sketch_csr";
+  }
+  // algorithmic bytes of one sketch of nv vectors of element size es
+  double prof_bytes(int nv, size_t es, long long G) const {
+    const double pbytes = 2.0 * nv * (double)slots(m, G) * ell * 8;  // partials written + read
+    if (kind == HS_SKETCH_SPARSE_SIGN) {
+      double eb = 2.0 * m * zeta;
+      {
+        std::lock_guard<std::mutex> g(lay_mu);
+        const auto it = layouts.find(tile_for(G));
+        if (it != layouts.end()) eb = 2.0 * it->second->nent;
+      }
+      return nv * (eb + (double)m * es) + pbytes;
+    }
+    if (kind == HS_SKETCH_DENSE) return nv * ((double)ell * m * 8 + (double)m * es) + pbytes;
+    if (kind == HS_SKETCH_GAUSSIAN) return nv * (double)m * es + pbytes;
+    return 0.0;
+  }
+
+  // z[:, w] = S v_w for nv vectors (column stride ldv; z column stride ldz)
+  // over the whole input cut in granules of G (the operator's shard granule;
+  // G = m: one granule), with `scratch` >= scratch_elems(nv, m, G) doubles.
+  // The Gaussian kind generates S once for the whole batch; per vector the
+  // result equals a single apply.
+  void apply_many(const void* v, int vdt, long long ldv, int nv, double* z, long long ldz, double* scratch,
+                  long long G, cudaStream_t st = nullptr) const {
+    cudaStream_t s = st ? st : ctx->stream;
+    if (nv <= 0) return;
+    Prof p(ctx, prof_name(), prof_bytes(nv, dsize(vdt), G), s);
+    if (kind == HS_SKETCH_CSR) {
+      const size_t es = dsize(vdt);
+      for (int w = 0; w < nv; ++w) {
+        const void* vw = reinterpret_cast<const char*>(v) + (size_t)w * ldv * es;
+        double* zw = z + (long long)w * ldz;
+        auto go = [&](auto tag) {
+          using Tin = decltype(tag);
+          sketch_csr_kernel<Tin><<<(int)ell, 256, 0, s>>>((int)ell, rowptr.as<long long>(), scol.as<int>(),
+                                                          cval.as<double>(), reinterpret_cast<const Tin*>(vw), zw);
+        };
+        if (vdt == HS_F64) go(double{});
+        else if (vdt == HS_F32) go(float{});
+        else go(__nv_bfloat16{});
+        CKL();
+      }
+      return;
+    }
+    if (!scratch) fail(HS_ERR_RUNTIME, "sketch apply without partial scratch");
+    const long long gpr = (m + G - 1) / G;
+    partials(v, vdt, ldv, nv, 0, m, G, scratch, slots(m, G), s);
+    reduce(scratch, nv, G, gpr, z, ldz, s);
+  }
+  void apply(const void* v, int vdt, double* z, double* scratch, long long G, cudaStream_t st = nullptr) const {
+    apply_many(v, vdt, 0, 1, z, 0, scratch, G, st);
   }
 };
+
+// Sparse-sign tile layout for tile size tc (hs_sketch.cuh:
+// sketch_sparse_gather_kernel): the entries (rows and signs from Philox,
+// sparse_sign_gen_kernel) are regenerated on the device and bucketed on the
+// host, per absolute tile of tc columns, by sketch row (columns ascending);
+// rows sorted by entry count (descending, ties by row), slices of 32 rows,
+// each slice padded to a multiple of 8 entries per lane and chunk-interleaved.
+const hs_sketch::SparseLayout& hs_sketch::sparse_layout(long long tc) const {
+  std::lock_guard<std::mutex> g(lay_mu);
+  auto it = layouts.find(tc);
+  if (it != layouts.end()) return *it->second;
+  if (tc > 8192 || tc < 1) fail(HS_ERR_VALUE, "sparse-sign tile %lld out of range", tc);
+  // entry = column offset (14 bits, the padding offset tc included) | sign bit 15
+  cudaStream_t s = ctx->stream;
+  const long long nnz = m * (long long)zeta;
+  std::vector<int> rows(nnz), scol(nnz);
+  {
+    DBuf dr(nnz * sizeof(int), false), ds(nnz * sizeof(int), false);
+    sparse_sign_gen_kernel<<<grid_for(m, 128, 1 << 30), 128, 0, s>>>(m, (int)ell, zeta, key(), dr.as<int>(),
+                                                                    ds.as<int>());
+    CKL();
+    CK(cudaMemcpyAsync(rows.data(), dr.p, nnz * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(scol.data(), ds.p, nnz * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  auto L = std::make_unique<SparseLayout>();
+  L->tc = tc;
+  L->ntiles = (m + tc - 1) / tc;
+  L->nsl = (int)((ell + 31) / 32);
+  const int nsl = L->nsl;
+  std::vector<long long> tbase(L->ntiles + 1, 0);
+  std::vector<int> soff((size_t)L->ntiles * (nsl + 1), 0);
+  std::vector<unsigned short> perm((size_t)L->ntiles * nsl * 32, 0xFFFF);
+  std::vector<unsigned short> ent;
+  ent.reserve((size_t)(nnz * 1.2) + 256);
+  std::vector<int> cnt(ell), order(ell), pos(ell), fill(ell);
+  for (long long k = 0; k < L->ntiles; ++k) {
+    const long long c0 = k * tc, c1 = std::min(m, c0 + tc);
+    std::fill(cnt.begin(), cnt.end(), 0);
+    for (long long c = c0; c < c1; ++c)
+      for (int j = 0; j < zeta; ++j) ++cnt[rows[c * zeta + j]];
+    for (int r = 0; r < ell; ++r) order[r] = r;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cnt[a] > cnt[b]; });
+    for (int p = 0; p < (int)ell; ++p) pos[order[p]] = p;
+    tbase[k] = (long long)ent.size();
+    int* so = soff.data() + (size_t)k * (nsl + 1);
+    int off = 0;
+    for (int sl = 0; sl < nsl; ++sl) {
+      so[sl] = off;
+      const int first = sl * 32;
+      const int len = first < ell ? cnt[order[first]] : 0;  // longest row of the slice
+      off += ((len + 7) / 8) * 256;
+      for (int l = 0; l < 32 && first + l < ell; ++l) perm[((size_t)k * nsl + sl) * 32 + l] = (unsigned short)order[first + l];
+    }
+    so[nsl] = off;
+    ent.resize(ent.size() + (size_t)off, (unsigned short)tc);  // padding reads the zero after the tile
+    std::fill(fill.begin(), fill.end(), 0);
+    for (long long c = c0; c < c1; ++c)
+      for (int j = 0; j < zeta; ++j) {
+        const int r = rows[c * zeta + j];
+        const int p = pos[r], sl = p / 32, lane = p % 32, e = fill[r]++;
+        const size_t idx = (size_t)tbase[k] + so[sl] + (size_t)(e / 8) * 256 + lane * 8 + e % 8;
+        ent[idx] = (unsigned short)((c - c0) | (scol[c * zeta + j] < 0 ? 0x8000 : 0));
+      }
+  }
+  tbase[L->ntiles] = (long long)ent.size();
+  L->nent = (long long)ent.size();
+  L->tbase.alloc(tbase.size() * sizeof(long long), false);
+  L->soff.alloc(soff.size() * sizeof(int), false);
+  L->perm.alloc(perm.size() * sizeof(unsigned short), false);
+  L->ent.alloc(std::max<size_t>(ent.size(), 8) * sizeof(unsigned short), false);
+  CK(cudaMemcpyAsync(L->tbase.p, tbase.data(), tbase.size() * sizeof(long long), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(L->soff.p, soff.data(), soff.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(L->perm.p, perm.data(), perm.size() * sizeof(unsigned short), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(L->ent.p, ent.data(), ent.size() * sizeof(unsigned short), cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  auto& ref = *L;
+  layouts.emplace(tc, std::move(L));
+  return ref;
+}
 
 // ---------------------------------------------------------------------------
 // result
@@ -1108,6 +1279,8 @@ struct Solver {
     const long long ell = skd ? S2->ell : (long long)K + 1;
     const bool lamon = cfg.lam > 0.0;
     const bool sb = cfg.sketch_basis != 0;
+    // sketch granules: S2 sketches range vectors, S1 domain vectors
+    const long long G2 = op->granule(0), G1 = op->granule(1);
     const bool printed = cfg.printed_f != 0 && !square && lamon && skd;  // slslu_tikhonov(printed_f_columns=True)
     const long long ldm = round_up(m, 64), ldn = round_up(n, 64);
     const int ldp = K + 2;
@@ -1317,17 +1490,21 @@ struct Solver {
       CK(cudaMemcpyAsync(Wcol(0), &w00d, sizeof(double), cudaMemcpyHostToDevice, s));
     }
     // sketch setup (solvers.py:454-463)
+    DBuf skinit;
     if (skd) {
-      S2->apply(r0.p, wdt, sr0.as<double>());
+      skinit.alloc((size_t)std::max<long long>({1LL, S2->scratch_elems(1, S2->m, G2), lamon && S1 ? S1->scratch_elems(1, S1->m, G1) : 0LL}) *
+                       sizeof(double),
+                   false);
+      S2->apply(r0.p, wdt, sr0.as<double>(), skinit.as<double>(), G2);
       sk0++;
       if (sb) {
-        S2->apply(first_basis, bdt, Gb.as<double>());
+        S2->apply(first_basis, bdt, Gb.as<double>(), skinit.as<double>(), G2);
         sk0++;
       }
       if (lamon) {
         // printed variant: the unreduced r = A^T d1 still in q (solvers.py:460-461)
-        if (printed) S1->apply(q.p, wdt, Fb.as<double>());
-        else S1->apply(Lcol(0), bdt, Fb.as<double>());
+        if (printed) S1->apply(q.p, wdt, Fb.as<double>(), skinit.as<double>(), G1);
+        else S1->apply(Lcol(0), bdt, Fb.as<double>(), skinit.as<double>(), G1);
         sk0++;
       }
     } else {
@@ -1424,6 +1601,7 @@ struct Solver {
     // Each z_k is bit-identical to the per-iteration sketch; only the fused
     // iterate lags (x_j rides on the basis pass of iteration j + 2*SB - 1,
     // the last ones are formed after the loop).
+    const bool sk_main = skd && S2 && S2->kind == HS_SKETCH_SPARSE_SIGN && !env_flag("HS_SK_AUX");
     const bool gauss_any = ovl && ((S2 && S2->kind == HS_SKETCH_GAUSSIAN) ||
                                    (lamon && S1 && S1->kind == HS_SKETCH_GAUSSIAN));
     int SB = 1;
@@ -1435,6 +1613,16 @@ struct Solver {
     const int xlag = SB > 1 ? 2 * SB - 1 : 1;
     DBuf uring(SB > 1 ? (size_t)2 * SB * ldm * sizeof(T) : 0);
     const int nbatch = (K + SB - 1) / SB;
+    // sketch partial scratch: one per stream the sketches run on (hs_sketch::apply_many)
+    auto skelems = [&](int nv) {
+      long long e = 0;
+      if (skd) e = std::max(e, S2->scratch_elems(nv, S2->m, G2));
+      if (skd && lamon && S1) e = std::max(e, S1->scratch_elems(nv, S1->m, G1));
+      return (size_t)std::max<long long>(e, 1);
+    };
+    DBuf skaux(skelems(SB) * sizeof(double), false), skmain(skelems(1) * sizeof(double), false);
+    double* const skA = skaux.as<double>();
+    double* const skM = skmain.as<double>();
     ev_skb = ctx->take_events(SB > 1 ? nbatch : 0, false);
     ev_qrb = ctx->take_events(SB > 1 ? nbatch : 0, false);
     std::vector<int> fused_at(K + 2, 0);  // iteration whose basis pass formed x_j
@@ -1447,9 +1635,9 @@ struct Solver {
       CK(cudaEventRecord(ev_l, s));
       CK(cudaStreamWaitEvent(s2, ev_l, 0));
       const long long slot0 = (long long)((kb0 - 1) % (2 * SB));
-      S2->apply_many(uring.as<T>() + slot0 * ldm, wdt, ldm, nb, Zb.as<double>() + (long long)(kb0 - 1) * ell, ell, s2);
+      S2->apply_many(uring.as<T>() + slot0 * ldm, wdt, ldm, nb, Zb.as<double>() + (long long)(kb0 - 1) * ell, ell, skA, G2, s2);
       CK(cudaEventRecord(ev_skb[bidx], s2));
-      if (lamon && !printed) S1->apply_many(Lcol(kb0), bdt, ldn, nb, Fb.as<double>() + (long long)kb0 * ell, ell, s2);
+      if (lamon && !printed) S1->apply_many(Lcol(kb0), bdt, ldn, nb, Fb.as<double>() + (long long)kb0 * ell, ell, skA, G1, s2);
       for (int kk = kb0; kk <= kend_b; ++kk) {
         qa.zcol = Zb.as<double>() + (long long)(kk - 1) * ell;
         qa.fcol = lamon ? Fb.as<double>() + (long long)(kk - 1) * ell : nullptr;
@@ -1501,9 +1689,20 @@ struct Solver {
       // A^T apply instead of competing with the D elimination pass for the SMs
       const bool defer_sk = ovl && SB == 1 && !square && !env_flag("HS_SK_EARLY");
       auto sketch_u = [&] {
+        if (sk_main) {
+          // a sparse-sign sketch is a ~10 us HBM stream: run it in order on
+          // the main stream rather than beside the A^T apply, whose L1-bound
+          // gathers lose when the sketch's 96 KB shared-memory blocks share
+          // their SMs
+          S2->apply(u.p, wdt, Zb.as<double>() + (long long)(k - 1) * ell, skM, G2);
+          CK(cudaEventRecord(ev_u, s));
+          CK(cudaStreamWaitEvent(s2, ev_u, 0));
+          CK(cudaEventRecord(ev_sk, s));
+          return;
+        }
         CK(cudaEventRecord(ev_u, s));
         CK(cudaStreamWaitEvent(s2, ev_u, 0));
-        S2->apply(u.p, wdt, Zb.as<double>() + (long long)(k - 1) * ell, s2);
+        S2->apply(u.p, wdt, Zb.as<double>() + (long long)(k - 1) * ell, skA, G2, s2);
         CK(cudaEventRecord(ev_sk, s2));
       };
       if (SB > 1) {
@@ -1513,10 +1712,10 @@ struct Solver {
       } else if (ovl) {
         CK(cudaEventRecord(ev_u, s));
         CK(cudaStreamWaitEvent(s2, ev_u, 0));
-        S2->apply(u.p, wdt, Zb.as<double>() + (long long)(k - 1) * ell, s2);
+        S2->apply(u.p, wdt, Zb.as<double>() + (long long)(k - 1) * ell, skA, G2, s2);
         CK(cudaEventRecord(ev_sk, s2));
       } else if (skd && !sb && !square) {  // serialised (diagnostics): sketch before the in-place elimination
-        S2->apply(u.p, wdt, Zb.as<double>() + (long long)(k - 1) * ell);
+        S2->apply(u.p, wdt, Zb.as<double>() + (long long)(k - 1) * ell, skM, G2);
       }
       // the fused iterate x_{k-1} needs y^{(k-1)} from the aux stream
       auto wait_y = [&] {
@@ -1540,10 +1739,10 @@ struct Solver {
                                                                           op->sblk, ybk);
         CKL();
         if (defer_sk) sketch_u();
-        if (sb) S2->apply(Dcol(k), bdt, Gb.as<double>() + (long long)k * ell);
+        if (sb) S2->apply(Dcol(k), bdt, Gb.as<double>() + (long long)k * ell, skM, G2);
         op->apply(Dcol(k), bdt, q.p, wdt, true, ybk != nullptr);
         // printed variant: F column k = S1 q before the elimination (solvers.py:488-490)
-        if (printed) S1->apply(q.p, wdt, Fb.as<double>() + (long long)k * ell);
+        if (printed) S1->apply(q.p, wdt, Fb.as<double>() + (long long)k * ell, skM, G1);
         fsub(q.as<T>(), gpos.as<long long>(), PL.as<T>(), ldp, k, k, 1, cvec.as<T>(), Wcol(k));
         wait_y();
         elim(q.as<T>(), n, ldn, L, k, 1, k, kx, yprev, relslot, q.as<T>());
@@ -1555,7 +1754,7 @@ struct Solver {
         normalize_kernel<T, B><<<grid_for(ldn, 256, NORM_G), 256, 0, s>>>(n, ldn, q.as<T>(), pv.as<T>() + 1, Lcol(k), st, 1, k);
         CKL();
       } else {
-        if (skd && !ovl && !sb) S2->apply(u.p, wdt, Zb.as<double>() + (long long)(k - 1) * ell);
+        if (skd && !ovl && !sb) S2->apply(u.p, wdt, Zb.as<double>() + (long long)(k - 1) * ell, skM, G2);
         fsub(ucur, tpos.as<long long>(), PL.as<T>(), ldp, k, k, 0, cvec.as<T>(), Hcol(k - 1));
         wait_y();
         elim(ucur, n, ldn, L, k, 0, k, kx, yprev, relslot, uel);
@@ -1569,7 +1768,7 @@ struct Solver {
                              cudaMemcpyDeviceToDevice, s));
         normalize_kernel<T, B><<<grid_for(ldn, 256, NORM_G), 256, 0, s>>>(n, ldn, uel, pv.as<T>(), Lcol(k), st, 0, k);
         CKL();
-        if (sb) S2->apply(Lcol(k), bdt, Gb.as<double>() + (long long)k * ell);
+        if (sb) S2->apply(Lcol(k), bdt, Gb.as<double>() + (long long)k * ell, skM, G2);
       }
       if (sb) {
         // M column k-1 = G[:, :k+1] @ H[:k+1, k-1]  (zero columns/entries past a breakdown)
@@ -1639,7 +1838,7 @@ struct Solver {
           CK(cudaEventRecord(ev_l, s));
           CK(cudaStreamWaitEvent(s2, ev_l, 0));
         }
-        if (skd) S1->apply(Lcol(k), bdt, Fb.as<double>() + (long long)k * ell, s2);
+        if (skd) S1->apply(Lcol(k), bdt, Fb.as<double>() + (long long)k * ell, skA, G1, s2);
       }
       CK(cudaEventRecord(ev[k], s));
       CK(cudaMemcpyAsync(hflag + k, &st->bd_iter, sizeof(int), cudaMemcpyDeviceToHost, s));

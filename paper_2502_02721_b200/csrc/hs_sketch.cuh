@@ -10,18 +10,103 @@
 
 namespace hs {
 
-// ---- explicit dense: one block per sketch row, fixed-tree block sum --------
-template <class Vs, class Tin>
+// ---- tiles ----------------------------------------------------------------
+// Every tiled sketch forms z = scale * sum over tiles (in order) of part_tile,
+// where part_tile is the sketch of the input entries of one tile, summed in an
+// order fixed by the tile's contents alone.  The input is cut into granules
+// of G entries -- the operator's shard granule: a row shard of the input is a
+// whole number of granules (hs_op::granule) -- and each granule into tiles of
+// tc entries (its last tile may be shorter).  The same partials, computed on
+// one GPU or spread over any number of ranks and all-gathered, therefore give
+// a bit-identical z (P-independent sketches).
+inline int ilog2_floor(long long x) {
+  int r = 0;
+  while (x > 1) {
+    x >>= 1;
+    ++r;
+  }
+  return r;
+}
+inline long long pow2_clamped(long long len, int shift, int lo, int hi) {
+  int e = (len >> shift) > 0 ? ilog2_floor(len >> shift) : 0;
+  e = e < lo ? lo : (e > hi ? hi : e);
+  return 1LL << e;
+}
+// columns per tile: sparse-sign ~len/128 (32..8192), Gaussian / dense ~len/1024 (256..8192)
+inline long long sketch_tile_sparse(long long len) { return pow2_clamped(len, 7, 5, 13); }
+inline long long sketch_tile_dense(long long len) { return pow2_clamped(len, 10, 8, 13); }
+// shard granule of a vector that may be split anywhere (tomography rays)
+inline long long shard_granule(long long len) { return pow2_clamped(len, 7, 8, 13); }
+
+// local tile b of a partial kernel: granule b / tpg, tile b % tpg of it, local
+// entries [c0, c1) (empty past the local length)
+struct TileMap {
+  long long G, tc, len;
+  int tpg;
+  __host__ __device__ void range(long long b, long long& c0, long long& c1) const {
+    const long long gs = (b / tpg) * G, t = b % tpg;
+    c0 = gs + t * tc;
+    const long long e = gs + ((t + 1) * tc < G ? (t + 1) * tc : G);
+    c1 = e < len ? e : len;
+    if (c0 > c1) c0 = c1;
+  }
+  __host__ __device__ long long slots() const { return ((len + G - 1) / G) * tpg; }
+};
+
+// z[w * ldz + i] = scale * the sum of all tile partials of the len inputs.
+// The partials are numbered f = q * tpg + t over the global granules q and
+// their tiles t (every granule but the last has tpg tiles); part holds blocks
+// of gpr granules, one per rank, each vector-major ([rank][w][slot][i]; on one
+// GPU gpr = all granules).  Block: 8 sketch rows x RPH phases; phase p sums
+// the partials f = p (mod RPH) in order, then the phases are added in order --
+// a fixed association that depends only on the global tile structure.
+constexpr int RPH = 32, RROWS = 8;
+__global__ void __launch_bounds__(RROWS * RPH)
+sketch_tile_reduce_kernel(int ell, long long len, long long G, long long tc, int tpg, long long gpr, int nv,
+                          const double* __restrict__ part, double scale, double* __restrict__ z, long long ldz) {
+  __shared__ double ph[RPH][RROWS + 1];
+  const int li = threadIdx.x % RROWS, p = threadIdx.x / RROWS;
+  const int i = blockIdx.x * RROWS + li;
+  const int w = blockIdx.y;
+  const long long nq = (len + G - 1) / G;
+  const long long glast = len - (nq - 1) * G;
+  const long long F = (nq - 1) * tpg + (glast + tc - 1) / tc;
+  double s = 0.0;
+  if (i < ell) {
+#pragma unroll 4
+    for (long long f = p; f < F; f += RPH) {
+      const long long q = f / tpg, t = f - q * tpg;
+      const long long r = q / gpr, ql = q - r * gpr;
+      s += __ldcg(part + (((r * nv + w) * gpr + ql) * tpg + t) * (long long)ell + i);
+    }
+  }
+  ph[p][li] = s;
+  __syncthreads();
+  if (p == 0 && i < ell) {
+    double a = ph[0][li];
+#pragma unroll
+    for (int k = 1; k < RPH; ++k) a += ph[k][li];
+    z[(long long)w * ldz + i] = a * scale;
+  }
+}
+
+// ---- explicit dense S (row-major, ld lds), one warp per sketch row of a tile:
+// lanes stride the tile's columns with fma, then a fixed xor-tree warp sum.
+// part[(w * tstride + t) * ell + i] for the single vector w = 0.
+template <class Tin>
 __global__ void __launch_bounds__(256)
-sketch_dense_kernel(int ell, long long m, const Vs* __restrict__ S, long long lds,
-                    const Tin* __restrict__ v, double* __restrict__ z) {
-  __shared__ double scratch[32];
-  const int i = blockIdx.x;
-  const Vs* row = S + (long long)i * lds;
+sketch_dense_tile_kernel(int ell, TileMap tm, long long col_offset, const double* __restrict__ S, long long lds,
+                         const Tin* __restrict__ v, double* __restrict__ part) {
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (i >= ell) return;
+  long long c0, c1;
+  tm.range(blockIdx.x, c0, c1);
+  const double* row = S + (long long)i * lds + col_offset;
   double acc = 0.0;
-  for (long long c = threadIdx.x; c < m; c += blockDim.x) acc = fma((double)row[c], cvt<double>(v[c]), acc);
-  acc = block_sum(acc, scratch);
-  if (threadIdx.x == 0) z[i] = acc;
+  for (long long c = c0 + lane; c < c1; c += 32) acc = fma(__ldg(row + c), cvt<double>(v[c]), acc);
+  acc = warp_sum(acc);
+  if (lane == 0) part[(long long)blockIdx.x * ell + i] = acc;
 }
 
 // ---- Gaussian from Philox: S[i, c] = N(seed; c, i) / sqrt(ell) -----------------
@@ -40,12 +125,12 @@ __device__ __forceinline__ void gauss_quad(uint2 key, unsigned long long c, unsi
 // one RNG pass instead of nv.  Per vector the columns each thread visits, the
 // fma order and the phase reduction do not depend on NV or nv, so a vector's
 // result is bit-identical whether it is sketched alone or in a batch.
-// part layout: part[(w * ntiles + tile) * ell + i].
+// part layout: part[(w * tstride + tile) * ell + i] (tstride >= local tiles).
 constexpr int GAUSS_CH = 1024;
 template <class Tin, int NV, int UNR = 2>
 __global__ void __launch_bounds__(256, 2)
-sketch_gauss_partial_kernel(int ell, long long m, long long col_offset, long long tile_cols, uint2 key,
-                            const Tin* __restrict__ v, long long ldv, int nv, double* __restrict__ part) {
+sketch_gauss_partial_kernel(int ell, TileMap tm, long long col_offset, uint2 key, const Tin* __restrict__ v,
+                            long long ldv, int nv, double* __restrict__ part, long long tstride) {
   extern __shared__ __align__(128) unsigned char gauss_smem[];
   double* vs = reinterpret_cast<double*>(gauss_smem);  // GAUSS_CH * NV
   __shared__ double red[256][4];
@@ -56,8 +141,8 @@ sketch_gauss_partial_kernel(int ell, long long m, long long col_offset, long lon
   const int ql = threadIdx.x % QB, ph = threadIdx.x / QB;
   const int q = blockIdx.y * QB + ql;
   const bool active = ph < PH && q < nq;
-  const long long c0 = (long long)blockIdx.x * tile_cols;
-  const long long c1 = min(m, c0 + tile_cols);
+  long long c0, c1;
+  tm.range(blockIdx.x, c0, c1);
   double a[NV][4];
 #pragma unroll
   for (int w = 0; w < NV; ++w) a[w][0] = a[w][1] = a[w][2] = a[w][3] = 0.0;
@@ -109,7 +194,7 @@ sketch_gauss_partial_kernel(int ell, long long m, long long col_offset, long lon
     red[threadIdx.x][2] = a[w][2]; red[threadIdx.x][3] = a[w][3];
     __syncthreads();
     if (ph == 0 && q < nq) {
-      double* pw = part + ((long long)w * gridDim.x + blockIdx.x) * ell;
+      double* pw = part + ((long long)w * tstride + blockIdx.x) * ell;
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const int i = 4 * q + r;
@@ -126,57 +211,36 @@ sketch_gauss_partial_kernel(int ell, long long m, long long col_offset, long lon
 // largest batch one partial launch handles
 constexpr int GAUSS_NV_MAX = 8;
 
-// launch the partial + reduce pair for nv vectors (column stride ldv) into
-// z[w * ldz + i]; batches larger than GAUSS_NV_MAX go in groups
+// partials of nv vectors (column stride ldv) over local columns [0, m) whose
+// first column is global column col_offset (a multiple of tile_cols):
+// part[(w * tstride + t) * ell + i]; batches larger than GAUSS_NV_MAX go in
+// groups.  Returns the number of launches.
 template <class Tin, int NV, int UNR = 2>
-inline void gauss_partial_launch(dim3 grid, cudaStream_t s, int ell, long long m, long long col_offset,
-                                 long long tile_cols, uint2 key, const Tin* v, long long ldv, int nv, double* part) {
+inline void gauss_partial_launch(dim3 grid, cudaStream_t s, int ell, TileMap tm, long long col_offset, uint2 key,
+                                 const Tin* v, long long ldv, int nv, double* part, long long tstride) {
   const size_t smem = (size_t)GAUSS_CH * NV * sizeof(double);
   ensure_smem((const void*)sketch_gauss_partial_kernel<Tin, NV, UNR>, smem);
-  sketch_gauss_partial_kernel<Tin, NV, UNR><<<grid, 256, smem, s>>>(ell, m, col_offset, tile_cols, key, v, ldv, nv,
-                                                                    part);
+  sketch_gauss_partial_kernel<Tin, NV, UNR><<<grid, 256, smem, s>>>(ell, tm, col_offset, key, v, ldv, nv, part,
+                                                                    tstride);
 }
 
-__global__ void sketch_tile_reduce_kernel(int ell, int ntiles, const double* __restrict__ part, double scale,
-                                          double* __restrict__ z, long long ldz);
-
 template <class Tin>
-inline int gauss_sketch_launch(cudaStream_t s, int ell, long long m, long long col_offset, long long tile_cols,
-                               uint2 key, const Tin* v, long long ldv, int nv, double* part, double* z,
-                               long long ldz) {
+inline int gauss_partials(cudaStream_t s, int ell, TileMap tm, long long col_offset, uint2 key, const Tin* v,
+                          long long ldv, int nv, double* part, long long tstride) {
   const int nq = (ell + 3) / 4;
-  const int ntl = (int)((m + tile_cols - 1) / tile_cols);
-  const dim3 grid(ntl, (nq + 63) / 64);
+  const dim3 grid((unsigned)tm.slots(), (nq + 63) / 64);
   int launches = 0;
   for (int w0 = 0; w0 < nv; w0 += GAUSS_NV_MAX) {
     const int g = nv - w0 < GAUSS_NV_MAX ? nv - w0 : GAUSS_NV_MAX;
     const Tin* vg = v + (long long)w0 * ldv;
-    if (g == 1) gauss_partial_launch<Tin, 1>(grid, s, ell, m, col_offset, tile_cols, key, vg, ldv, g, part);
-    else if (g == 2) gauss_partial_launch<Tin, 2>(grid, s, ell, m, col_offset, tile_cols, key, vg, ldv, g, part);
-    else if (g <= 4) gauss_partial_launch<Tin, 4>(grid, s, ell, m, col_offset, tile_cols, key, vg, ldv, g, part);
-    else gauss_partial_launch<Tin, 8>(grid, s, ell, m, col_offset, tile_cols, key, vg, ldv, g, part);
-    sketch_tile_reduce_kernel<<<dim3((ell + 127) / 128, g), 128, 0, s>>>(ell, ntl, part, 1.0 / sqrt((double)ell),
-                                                                         z + (long long)w0 * ldz, ldz);
-    launches += 2;
+    double* pg = part + (long long)w0 * tstride * ell;
+    if (g == 1) gauss_partial_launch<Tin, 1>(grid, s, ell, tm, col_offset, key, vg, ldv, g, pg, tstride);
+    else if (g == 2) gauss_partial_launch<Tin, 2>(grid, s, ell, tm, col_offset, key, vg, ldv, g, pg, tstride);
+    else if (g <= 4) gauss_partial_launch<Tin, 4>(grid, s, ell, tm, col_offset, key, vg, ldv, g, pg, tstride);
+    else gauss_partial_launch<Tin, 8>(grid, s, ell, tm, col_offset, key, vg, ldv, g, pg, tstride);
+    ++launches;
   }
   return launches;
-}
-
-// number of row-quad blocks for the partial kernel (<= 64 quads per block, balanced)
-inline int gauss_quad_blocks(int ell) {
-  const int nq = (ell + 3) / 4;
-  return (nq + 63) / 64;
-}
-
-// z[w * ldz + i] = scale * sum_t part[w][t][i]   (t ascending); grid.y = vector
-__global__ void sketch_tile_reduce_kernel(int ell, int ntiles, const double* __restrict__ part, double scale,
-                                          double* __restrict__ z, long long ldz) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= ell) return;
-  const double* pw = part + (long long)blockIdx.y * ntiles * ell;
-  double s = 0.0;
-  for (int t = 0; t < ntiles; ++t) s += pw[(long long)t * ell + i];
-  z[(long long)blockIdx.y * ldz + i] = s * scale;
 }
 
 // materialise the generated Gaussian S (row-major ell x m, fp64) for export
@@ -222,25 +286,96 @@ __global__ void sparse_sign_gen_kernel(long long m, int ell, int zeta, uint2 key
   }
 }
 
-// z[i] = scale * sum over row i's entries (+-) v[col]; block per sketch row
-template <class Tin>
+// Sparse-sign partials of one tile.  The scatter-add z_r += s_rc v_c of the
+// tile's entries is resolved at build time (hs_sketch::sparse_layout): per
+// absolute tile of tc columns, the sketch rows are sorted by their entry count
+// and cut into slices of 32, and lane r of a slice holds its row's entries in
+// column order, 8 per 16-byte chunk -- entry e at chunk-interleaved position
+// (e / 8) * 256 + r * 8 + e % 8, so a warp streams 512 contiguous bytes per
+// chunk.  Entry = column offset in the tile (bits 0-13) | 0x8000 if negative;
+// padding = offset tc, which reads the zero after the staged tile.  The CTA
+// stages the tile of v in shared memory as fp64; each lane then adds its
+// row's +-v (sign by xor of the high word) into four register accumulators
+// (entry e into a[e % 4]), combined as (a0 + a1) + (a2 + a3).  No atomics;
+// the order is fixed by the layout, so the partial is deterministic.
+// The tile size tm.tc must divide the granule and the column offset.
+template <class Tin> struct SkStage { using T = float; };   // staged tile type (bf16, fp32: exact in fp32)
+template <> struct SkStage<double> { using T = double; };
+
+// grid (local tile slots, slice groups of 8); warp w of block (b, y) adds
+// slice 8 y + w of tile b
+template <class Tin, int CB>
 __global__ void __launch_bounds__(256)
-sketch_sparse_kernel(int ell, const long long* __restrict__ rowptr, const int* __restrict__ scol,
-                     long long col_offset, long long m_loc, const Tin* __restrict__ v, double scale,
-                     double* __restrict__ z) {
-  __shared__ double scratch[32];
-  const int i = blockIdx.x;
-  double acc = 0.0;
-  for (long long p = rowptr[i] + threadIdx.x; p < rowptr[i + 1]; p += blockDim.x) {
-    const int sc = scol[p];
-    const long long c = (long long)(sc < 0 ? -sc : sc) - 1 - col_offset;
-    if (c >= 0 && c < m_loc) {
-      const double x = cvt<double>(v[c]);
-      acc += sc < 0 ? -x : x;
+sketch_sparse_gather_kernel(int ell, int nsl, TileMap tm, long long col_offset, const long long* __restrict__ tbase,
+                            const int* __restrict__ soff, const unsigned short* __restrict__ perm,
+                            const unsigned short* __restrict__ ent, const Tin* __restrict__ v,
+                            double* __restrict__ part) {
+  using S = typename SkStage<Tin>::T;
+  extern __shared__ __align__(16) unsigned char sk_smem[];
+  S* vs = reinterpret_cast<S*>(sk_smem);  // tc + 1 values
+  long long c0, c1;
+  tm.range(blockIdx.x, c0, c1);
+  if (c1 <= c0) return;  // empty slot past the local length (never reduced)
+  const long long k = (col_offset + c0) / tm.tc;  // absolute tile
+  const int n = (int)(c1 - c0), tc = (int)tm.tc;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sl = blockIdx.y * 8 + warp;
+  const bool active = sl < nsl;
+  // this warp's slice bounds and output rows, fetched before the staging
+  const int* so = soff + k * (nsl + 1);
+  const int a = active ? so[sl] : 0, L8 = active ? (so[sl + 1] - a) >> 8 : 0;
+  const unsigned r = active ? perm[(k * nsl + sl) * 32 + lane] : 0xFFFFu;
+  const uint4* ep = reinterpret_cast<const uint4*>(ent + tbase[k] + a) + lane;
+  // stage the tile: all of a thread's loads issued before any store
+  for (int i0 = 0; i0 <= tc; i0 += 16 * 256) {
+    S t[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int i = i0 + u * 256 + (int)threadIdx.x;
+      t[u] = i < n ? cvt<S>(__ldcs(v + c0 + i)) : S(0);
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int i = i0 + u * 256 + (int)threadIdx.x;
+      if (i <= tc) vs[i] = t[u];
     }
   }
-  acc = block_sum(acc, scratch);
-  if (threadIdx.x == 0) z[i] = acc * scale;
+  __syncthreads();
+  if (!active) return;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  const unsigned pad = (unsigned)tc | ((unsigned)tc << 16);
+  for (int q0 = 0; q0 < L8; q0 += CB) {
+    uint4 w[CB];
+#pragma unroll
+    for (int q = 0; q < CB; ++q)
+      w[q] = q0 + q < L8 ? __ldcs(ep + (long long)(q0 + q) * 32) : make_uint4(pad, pad, pad, pad);
+#pragma unroll
+    for (int q = 0; q < CB; ++q) {
+      const unsigned u4[4] = {w[q].x, w[q].y, w[q].z, w[q].w};
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        const unsigned e = (u4[h >> 1] >> ((h & 1) * 16)) & 0xFFFFu;
+        const double x = (double)vs[e & 0x3FFFu];
+        const long long sg = (long long)(e & 0x8000u) << 48;  // sign bit -> bit 63
+        acc[h & 3] += __longlong_as_double(__double_as_longlong(x) ^ sg);
+      }
+    }
+  }
+  if (r != 0xFFFFu) part[(long long)blockIdx.x * ell + r] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+}
+
+template <class Tin>
+inline void sparse_partials(cudaStream_t s, int ell, TileMap tm, long long col_offset, const long long* tbase,
+                            const int* soff, const unsigned short* perm, const unsigned short* ent, const Tin* v,
+                            double* part) {
+  const long long nt = tm.slots();
+  if (nt == 0) return;
+  const int nsl = (ell + 31) / 32;
+  const size_t smem = (size_t)(tm.tc + 1) * sizeof(typename SkStage<Tin>::T);
+  auto kern = sketch_sparse_gather_kernel<Tin, 8>;
+  ensure_smem((const void*)kern, smem);
+  kern<<<dim3((unsigned)nt, (unsigned)((nsl + 7) / 8)), 256, smem, s>>>(ell, nsl, tm, col_offset, tbase, soff, perm,
+                                                                       ent, v, part);
 }
 
 // ---- general explicit sparse S (CSR by sketch rows, fp64 values) ------------

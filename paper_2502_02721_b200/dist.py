@@ -23,7 +23,7 @@ from dataclasses import dataclass
 
 from . import _lib
 
-__all__ = ["ShardPlan", "shard_plan", "psf_shard_plan", "init_comm", "comm_info"]
+__all__ = ["ShardPlan", "shard_plan", "psf_shard_plan", "shard_granule", "sketch_tile", "init_comm", "comm_info"]
 
 
 def _round_up(a, b):
@@ -40,11 +40,31 @@ class ShardPlan:
     n_blk: int
 
 
+def _pow2_clamped(length, shift, lo, hi):
+    e = (length >> shift).bit_length() - 1 if (length >> shift) > 0 else 0
+    return 1 << min(hi, max(lo, e))
+
+
+def sketch_tile(kind, length):
+    """Columns per sketch partial tile (hs_sketch.cuh): sparse-sign ~len/128
+    in [32, 8192], Gaussian / dense ~len/1024 in [256, 8192]."""
+    if kind == "sparse_sign":
+        return _pow2_clamped(length, 7, 5, 13)
+    return _pow2_clamped(length, 10, 8, 13)
+
+
+def shard_granule(length):
+    """Ray blocks (rows of a tomography operator) are multiples of this power
+    of two; image shards are multiples of 8 rows.  Sketches sum their tile
+    partials granule by granule (hs_sketch.cuh), so they are P-independent."""
+    return _pow2_clamped(length, 7, 8, 13)
+
+
 def shard_plan(grid, n_angles, n_bins, nranks, rank):
     """Row blocks of rank ``rank`` for a grid^2-pixel, n_angles*n_bins-ray
-    operator (same arithmetic as the C library)."""
+    operator (same arithmetic as the C library, hs_dist.inc:build_tomo_sharded)."""
     m, n = n_angles * n_bins, grid * grid
-    m_blk = _round_up(-(-m // nranks), 64)
+    m_blk = _round_up(-(-m // nranks), max(64, shard_granule(m)))
     m_off = rank * m_blk
     m_loc = max(0, min(m_blk, m - m_off))
     rows_pr = _round_up(-(-grid // nranks), 8)
