@@ -116,6 +116,13 @@ int hs_ctx_synchronize(hs_ctx* ctx);
 int hs_comm_get_unique_id(void* out_128_bytes);
 int hs_comm_init(hs_ctx* ctx, int nranks, int rank, const void* unique_id_128_bytes);
 int hs_comm_info(const hs_ctx* ctx, int32_t* nranks, int32_t* rank);
+/* in-process ranks: contexts ctxs[0..nranks) become ranks 0..nranks-1 of one
+   communicator whose collectives are stream-ordered device copies between the
+   contexts (one host thread per rank drives its solve).  Same partition and
+   message sequence as the NCCL path; used to run P-rank solves on one GPU. */
+int hs_comm_init_local(hs_ctx** ctxs, int nranks);
+/* release every in-process rank blocked in (or entering) a collective: they fail with HS_ERR_COMM */
+int hs_comm_abort(hs_ctx* ctx);
 /* test hook: build operators / run solves through the sharded path with one rank */
 int hs_ctx_force_sharding(hs_ctx* ctx, int on);
 /* after hs_comm_init with nranks > 1, hs_op_tomo_create builds only this

@@ -63,6 +63,8 @@ _SIGNATURES = [
     ("hs_comm_get_unique_id", c_i32, [c_vp]),
     ("hs_comm_init", c_i32, [c_vp, ctypes.c_int, ctypes.c_int, c_vp]),
     ("hs_comm_info", c_i32, [c_vp, P_i32, P_i32]),
+    ("hs_comm_init_local", c_i32, [ctypes.POINTER(c_vp), ctypes.c_int]),
+    ("hs_comm_abort", c_i32, [c_vp]),
     ("hs_ctx_force_sharding", c_i32, [c_vp, ctypes.c_int]),
     ("hs_op_shard_info", c_i32, [c_vp, P_i64, P_i64, P_i64, P_i64, P_i64, P_i64]),
     ("hs_op_dense_create", c_i32, [c_vp, c_i64, c_i64, c_vp, ctypes.c_int, ctypes.POINTER(c_vp)]),
@@ -177,6 +179,12 @@ class Context:
     def synchronize(self):
         check(self._lib.hs_ctx_synchronize(self.handle))
 
+    def close(self):
+        """Destroy the context (objects created on it keep their buffers valid)."""
+        h, self.handle = self.handle, None
+        if h is not None:
+            check(self._lib.hs_ctx_destroy(h))
+
     def set_profiling(self, on):
         check(self._lib.hs_ctx_set_profiling(self.handle, 1 if on else 0))
 
@@ -197,10 +205,32 @@ class Context:
 
 
 _ctx = {}
+_tls = threading.local()
+
+
+class use_context:
+    """``with use_context(ctx):`` -- objects created and solves run on this
+    thread use ``ctx`` instead of the process-wide context (one host thread per
+    in-process rank, :func:`paper_2502_02721_b200.dist.local_group`)."""
+
+    def __init__(self, ctx):
+        self.ctx = ctx
+
+    def __enter__(self):
+        self.prev = getattr(_tls, "ctx", None)
+        _tls.ctx = self.ctx
+        return self.ctx
+
+    def __exit__(self, *exc):
+        _tls.ctx = self.prev
 
 
 def context(device=None):
-    """The process-wide context for ``device`` (default: LOCAL_RANK or 0)."""
+    """The context of this thread (:class:`use_context`), else the
+    process-wide context for ``device`` (default: LOCAL_RANK or 0)."""
+    over = getattr(_tls, "ctx", None)
+    if over is not None and (device is None or int(device) == over.device):
+        return over
     if device is None:
         device = int(os.environ.get("HS_DEVICE", os.environ.get("LOCAL_RANK", "0")))
     with _lock:

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <array>
 #include <atomic>
+#include <condition_variable>
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
@@ -75,6 +76,7 @@ static std::atomic<unsigned long long> g_launches{0};  // kernels launched by th
 
 template <class F>
 int guarded(F&& f) {
+  (void)cudaGetLastError();  // a stale error of an unrelated earlier call is not this call's
   try {
     f();
     return HS_OK;
@@ -201,6 +203,7 @@ struct hs_ctx {
   int num_sms = 148;
   int nranks = 1, rank = 0;
   void* comm = nullptr;  // ncclComm_t when nranks > 1 (hs_dist.inc)
+  std::shared_ptr<struct LocalComm> lcomm;  // in-process ranks (hs_comm_init_local), instead of NCCL
   bool force_shard = false;  // run the sharded operator/loop even with one rank (tests)
   bool profiling = false;
   std::map<std::string, KStat> stats;
@@ -536,6 +539,7 @@ static void csr_to_sell(hs_ctx* ctx, const Csr& A, Sell& S, int tile_grid = 0) {
 
 struct hs_op {
   hs_ctx* ctx = nullptr;
+  int device = 0;
   int kind = OP_DENSE;
   int vdtype = HS_F64;
   long long m = 0, n = 0;
@@ -922,6 +926,7 @@ static void csr_transpose(hs_ctx* ctx, const Csr& src, long long row_offset, lon
 
 struct hs_sketch {
   hs_ctx* ctx = nullptr;
+  int device = 0;
   int kind = HS_SKETCH_DENSE;
   long long ell = 0, m = 0;
   unsigned long long seed = 0;
@@ -1162,6 +1167,7 @@ struct hs_result {
   std::shared_ptr<DBuf> xdev;
   long long ldn = 0, ldm = 0;
   hs_ctx* ctx = nullptr;
+  int device = 0;
   // sharded solves keep only this rank's rows of the bases
   bool sharded = false;
   long long n_loc = 0, m_loc = 0;

@@ -23,7 +23,8 @@ from dataclasses import dataclass
 
 from . import _lib
 
-__all__ = ["ShardPlan", "shard_plan", "psf_shard_plan", "shard_granule", "sketch_tile", "init_comm", "comm_info"]
+__all__ = ["ShardPlan", "shard_plan", "psf_shard_plan", "shard_granule", "sketch_tile", "init_comm", "comm_info",
+           "local_group", "run_ranks"]
 
 
 def _round_up(a, b):
@@ -119,3 +120,46 @@ def force_sharding(on=True, ctx=None):
     """Test hook: route operators / solves through the sharded path with one rank."""
     ctx = ctx or _lib.context()
     _lib.check(_lib.load().hs_ctx_force_sharding(ctx.handle, 1 if on else 0))
+
+
+def local_group(nranks, devices=None):
+    """``nranks`` in-process ranks: one new context per rank (on ``devices[r]``,
+    default all on the current device) joined by the library's in-process
+    communicator (hs_comm_init_local: the NCCL path's partition and message
+    sequence, with stream-ordered device copies between the contexts).
+    Drive them with :func:`run_ranks`; close the contexts when done."""
+    if devices is None:
+        devices = [_lib.context().device] * nranks
+    if len(devices) != nranks:
+        raise ValueError("one device per rank")
+    ctxs = [_lib.Context(d) for d in devices]
+    arr = (_lib.c_vp * nranks)(*[c.handle for c in ctxs])
+    _lib.check(_lib.load().hs_comm_init_local(arr, nranks))
+    return ctxs
+
+
+def run_ranks(fn, ctxs):
+    """Run ``fn(rank, ctx)`` on one host thread per rank (each under
+    ``_lib.use_context(ctx)``) and return the per-rank results; the first
+    exception is re-raised after every thread has finished."""
+    import threading
+
+    out, err = [None] * len(ctxs), [None] * len(ctxs)
+
+    def body(r):
+        try:
+            with _lib.use_context(ctxs[r]):
+                out[r] = fn(r, ctxs[r])
+        except BaseException as e:  # noqa: BLE001 -- re-raised below
+            err[r] = e
+            _lib.load().hs_comm_abort(ctxs[r].handle)  # release the peers' collectives
+
+    threads = [threading.Thread(target=body, args=(r,)) for r in range(len(ctxs))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for e in err:
+        if e is not None:
+            raise e
+    return out

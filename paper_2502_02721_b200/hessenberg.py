@@ -106,7 +106,7 @@ class DeviceFactorization:
     """Host view of the device factorization A L_k = L_{k+1} H (square) or
     A L_k = D_{k+1} H, A^T D_{k+1} = L_{k+1} W (rectangular)."""
 
-    def __init__(self, result, square, rows, cols):
+    def __init__(self, result, square, rows, cols, basis_rows=None):
         from . import _lib
 
         self._res = result  # keeps the native result (and device bases) alive
@@ -127,8 +127,11 @@ class DeviceFactorization:
                 return out
             return f
 
-        self.L_cols = _LazyCols(fetch(0, cols), info["n_basis_sol"])
-        self.D_cols = None if square else _LazyCols(fetch(1, rows), info["n_basis_data"])
+        # basis_rows: (data, solution) rows held here -- this rank's shard of a
+        # row-sharded solve (hs_dist.inc), the full length otherwise
+        d_len, l_len = basis_rows if basis_rows is not None else (rows, cols)
+        self.L_cols = _LazyCols(fetch(0, l_len), info["n_basis_sol"])
+        self.D_cols = None if square else _LazyCols(fetch(1, d_len), info["n_basis_data"])
         self._tfull = None
         self._gfull = None
 

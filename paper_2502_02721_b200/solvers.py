@@ -354,7 +354,10 @@ def _hessenberg_solve(A, b, cfg, x_true, square, sketch_basis, sketch=None, S1=N
             matvecs=int(nr.matvecs[i]), tmatvecs=int(nr.tmatvecs[i]), dots=int(nr.dots[i]),
             sketches=int(nr.sketches[i]), wall_ms=float(nr.wall[i]), rank_fallback=bool(nr.rankfb[i]),
         ))
-    fact = DeviceFactorization(nr, square, A.rows, A.cols)
+    # a row-sharded solve keeps this rank's rows of the bases (hs_op_shard_info)
+    loc = [_lib.c_i64() for _ in range(6)]
+    _lib.check(_lib.load().hs_op_shard_info(dev.handle, *[ctypes.byref(v) for v in loc]))
+    fact = DeviceFactorization(nr, square, A.rows, A.cols, basis_rows=(loc[1].value, loc[4].value))
     return SolveResult(x=nr.x, trace=trace, termination=term, factorization=fact, loop_ms=nr.loop_ms)
 
 
