@@ -457,3 +457,90 @@ void co_spmv_f32_f64(int64_t rows, const int64_t* rp, const int32_t* ci, const f
     y[i] = acc;
   }
 }
+
+/* ---- square process on the PSF operator (BASELINE config 5, fp32 storage) ----
+   out[r, c] = sum over a (outer), b (inner) of K[a, b] * x[r + ry - a, c + rx - b]
+   (zero outside; each product rounded, then added to the running sum from +0):
+   the order-specified stencil of oracle/tomo_oracle.py:psf_stencil (transpose
+   = False), which the device stencil reproduces bit for bit. */
+static void psf_conv_f32(int Hh, int Ww, const float* K, int kh, int kw, const float* x, float* out, int T) {
+  const int ry = kh / 2, rx = kw / 2;
+#pragma omp parallel num_threads(T)
+  {
+    float* acc = (float*)malloc(sizeof(float) * (size_t)Ww);
+#pragma omp for schedule(static)
+    for (int r = 0; r < Hh; ++r) {
+      for (int c = 0; c < Ww; ++c) acc[c] = 0.0f;
+      for (int a = 0; a < kh; ++a) {
+        const int rr = r + ry - a;
+        for (int b = 0; b < kw; ++b) {
+          const float kab = K[a * kw + b];
+          const int off = rx - b;
+          if (rr < 0 || rr >= Hh) {
+            /* zero row: every product is +0 or -0 times kab; acc + (+-0) keeps acc
+               unless acc is -0, which it never is (it starts at +0) */
+            continue;
+          }
+          const float* xr = x + (size_t)rr * Ww;
+          const int c0 = off < 0 ? -off : 0, c1 = Ww - (off > 0 ? off : 0);
+          for (int c = 0; c < c0; ++c) acc[c] = acc[c] + kab * 0.0f;
+          for (int c = c0; c < c1; ++c) {
+            float prod = kab * xr[c + off];
+            acc[c] = acc[c] + prod;
+          }
+          for (int c = c1; c < Ww; ++c) acc[c] = acc[c] + kab * 0.0f;
+        }
+      }
+      memcpy(out + (size_t)r * Ww, acc, sizeof(float) * (size_t)Ww);
+    }
+    free(acc);
+  }
+}
+
+void co_psf_conv_f32(int Hh, int Ww, const float* K, int kh, int kw, const float* x, float* out, int nthreads) {
+  psf_conv_f32(Hh, Ww, K, kh, kw, x, out, nthreads > 0 ? nthreads : omp_get_max_threads());
+}
+
+/* hessenberg.py:160-226 (full pivoting), float32 vectors and basis: pivots t
+   (maxiter + 1) and H columns (h_out[j * (maxiter + 1) + i], column-major).
+   Returns the number of steps done. */
+int co_scmrh_psf_f32(int Hh, int Ww, const float* K, int kh, int kw, const double* b, int maxiter, int nthreads,
+                     int64_t* t_out, double* h_out) {
+  const int T = nthreads > 0 ? nthreads : omp_get_max_threads();
+  const int64_t n = (int64_t)Hh * Ww;
+  const int KK = maxiter;
+  float** L = (float**)calloc((size_t)KK + 2, sizeof(float*));
+  int64_t* t = (int64_t*)calloc((size_t)KK + 2, sizeof(int64_t));
+  double* hcol = (double*)calloc((size_t)KK + 2, sizeof(double));
+  float* u = (float*)malloc(sizeof(float) * (size_t)n);
+  int64_t idx;
+  float val;
+  int done = 0;
+  for (int64_t i = 0; i < n; ++i) u[i] = (float)b[i];
+  argmax_abs(u, n, &idx, &val, T);
+  if (val == 0.0f) goto out2;
+  t[0] = idx;
+  L[0] = (float*)malloc(sizeof(float) * (size_t)n);
+  for (int64_t i = 0; i < n; ++i) L[0][i] = u[i] / val;
+  for (int k = 1; k <= KK; ++k) {
+    psf_conv_f32(Hh, Ww, K, kh, kw, L[k - 1], u, T);
+    for (int i = 0; i <= KK; ++i) hcol[i] = 0.0;
+    eliminate(u, n, L, t, k, hcol, T);
+    argmax_abs(u, n, &idx, &val, T);
+    const int bd = (k >= n || val == 0.0f);
+    hcol[k] = bd ? 0.0 : (double)val;
+    if (h_out) memcpy(h_out + (size_t)(k - 1) * (KK + 1), hcol, sizeof(double) * ((size_t)KK + 1));
+    done = k;
+    if (bd) break;
+    t[k] = idx;
+    L[k] = (float*)malloc(sizeof(float) * (size_t)n);
+    float* lk = L[k];
+#pragma omp parallel for schedule(static) num_threads(T)
+    for (int64_t i = 0; i < n; ++i) lk[i] = u[i] / val;
+  }
+out2:
+  if (t_out) memcpy(t_out, t, sizeof(int64_t) * ((size_t)KK + 1));
+  for (int i = 0; i <= KK + 1; ++i) free(L[i]);
+  free(L); free(t); free(hcol); free(u);
+  return done;
+}

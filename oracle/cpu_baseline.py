@@ -39,6 +39,9 @@ def lib():
         _lib.co_max_threads.restype = ctypes.c_int
         _lib.co_spmv_f32_f64.argtypes = [i64, vp, vp, vp, vp, vp, i32]
         _lib.co_spmv_f32_export.argtypes = [i64, vp, vp, vp, vp, vp, i32]
+        _lib.co_psf_conv_f32.argtypes = [i32, i32, vp, i32, i32, vp, vp, i32]
+        _lib.co_scmrh_psf_f32.argtypes = [i32, i32, vp, i32, i32, vp, i32, i32, vp, vp]
+        _lib.co_scmrh_psf_f32.restype = ctypes.c_int
     return _lib
 
 
@@ -151,3 +154,26 @@ def run(w, budget_s=20.0, nthreads=None, b=None):
                    f"{r['done']} of {K} iterations in {sum(r['iter_s']):.1f}s, rate extrapolated to {K} iterations "
                    f"with t(k)={a:.3f}+{bb:.5f}k s; host operator build {build_s:.1f}s"),
     }
+
+
+def psf_conv(img, kernel, nthreads=None):
+    """Order-specified zero-boundary convolution (tomo_oracle.psf_stencil,
+    transpose=False) of a float32 image, in C."""
+    img = np.ascontiguousarray(img, dtype=np.float32)
+    K = np.ascontiguousarray(kernel, dtype=np.float32)
+    out = np.empty_like(img)
+    lib().co_psf_conv_f32(img.shape[0], img.shape[1], _p(K), K.shape[0], K.shape[1], _p(img), _p(out),
+                          nthreads or os.cpu_count())
+    return out
+
+
+def scmrh_psf_pivots(shape, kernel, b, maxiter, nthreads=None):
+    """The square Hessenberg process (hessenberg.py:160-226) on the PSF
+    operator with float32 vectors and basis, in C: (pivots t[:done+1], H)."""
+    K = np.ascontiguousarray(kernel, dtype=np.float32)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    t = np.zeros(maxiter + 1, dtype=np.int64)
+    h = np.zeros((maxiter, maxiter + 1))
+    done = lib().co_scmrh_psf_f32(shape[0], shape[1], _p(K), K.shape[0], K.shape[1], _p(b), maxiter,
+                                  nthreads or os.cpu_count(), _p(t), _p(h))
+    return t[: done + 1], np.ascontiguousarray(h[:done].T)

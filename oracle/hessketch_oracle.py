@@ -8,6 +8,16 @@ the working precision ``dtype``:
 * ``np.float64`` -- the reference itself.  With the same operator callables and
   the same sketch matrices it reproduces the reference bit for bit (pinned by
   ``tests/test_oracle_golden.py`` against fixtures generated from the reference).
+* ``storage="bfloat16"`` (with ``np.float32``) -- the basis columns are
+  *stored* in bfloat16: each normalised column is rounded to nearest-even
+  bf16 when it is appended, and everything that reads the basis afterwards
+  (the operator input A l_k, the in-order elimination, x = L_k y) reads the
+  stored values.  This is the device's bf16-storage path (BASELINE config 5:
+  "basis vectors stored in bf16 with fp32 pivoting, axpy and sketch
+  accumulation"); the reference has no counterpart.  Partial pivoting keeps
+  the pivot entry exactly 1.0 and earlier pivot rows exactly 0.0 in bf16, so
+  the coefficients read from u at the pivots are still the forward
+  substitution on the stored pivot rows.
 * ``np.float32`` -- "oracle32": identical algorithm, but the Krylov vectors
   (r0, u, q, basis columns) and the elimination / pivot / normalisation
   arithmetic are float32, as the device's fp32 path computes them.  Sketch
@@ -214,7 +224,21 @@ class SquareState:
         return H if rows is None else H[:rows]
 
 
-def init_square(A, b, x0=None, sample_size=0, rng=None):
+def round_bf16(a):
+    """Round float32 values to the nearest bfloat16 (ties to even), returned as
+    float32 -- the device's __float2bfloat16_rn storage conversion."""
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    bits = a.view(np.uint32).astype(np.uint64)
+    bits = (bits + 0x7FFF + ((bits >> 16) & 1)) & 0xFFFF0000
+    return bits.astype(np.uint32).view(np.float32)
+
+
+def _store(v, storage):
+    """A new basis column as the basis stores it."""
+    return round_bf16(v) if storage == "bfloat16" else v
+
+
+def init_square(A, b, x0=None, sample_size=0, rng=None, storage=None):
     """hessenberg.py:160-188 (full or sampled pivoting)."""
     if not A.is_square:
         raise ValueError("the square Hessenberg process needs a square operator")
@@ -229,8 +253,9 @@ def init_square(A, b, x0=None, sample_size=0, rng=None):
         x = np.zeros(A.cols) if x0 is None else np.asarray(x0, dtype=np.float64).copy()
         raise TrivialSolution("initial residual is zero; starting point is exact", x)
     _swap_to_position(t, 0, idx)
-    st = SquareState([r0 / beta], [], t, beta, 0, False, r0)
+    st = SquareState([_store(r0 / beta, storage)], [], t, beta, 0, False, r0)
     st.sample_size, st.rng = sample_size, rng
+    st.storage = storage
     return st
 
 
@@ -265,7 +290,7 @@ def step_square(state, A, keep_product=True):
     else:
         h[k] = val
         _swap_to_position(state.t, k, idx)
-        state.L.append(u / val)
+        state.L.append(_store(u / val, getattr(state, "storage", None)))
     state.h_cols.append(h)
     state.k = k
     return state
@@ -308,7 +333,7 @@ class GenState:
         return W if rows is None else W[:rows]
 
 
-def init_generalized(A, b, x0=None, sample_size=0, rng=None):
+def init_generalized(A, b, x0=None, sample_size=0, rng=None, storage=None):
     """hessenberg.py:275-326 (full or sampled pivoting)."""
     dt = A.dtype
     b = np.asarray(b, dtype=dt)
@@ -320,7 +345,7 @@ def init_generalized(A, b, x0=None, sample_size=0, rng=None):
     idx, beta = pivot_with_fallback(r0, t, sample_size, rng)
     if beta == 0.0:
         raise TrivialSolution("initial residual is zero; starting point is exact", zero_x)
-    d1 = r0 / beta
+    d1 = _store(r0 / beta, storage)
     _swap_to_position(t, 0, idx)
     v0 = A.apply_transpose(r0)
     g = np.arange(A.cols)
@@ -329,13 +354,14 @@ def init_generalized(A, b, x0=None, sample_size=0, rng=None):
         raise TrivialSolution(
             "transposed residual is zero; the normal equations already hold", zero_x
         )
-    l1 = v0 / alpha
+    l1 = _store(v0 / alpha, storage)
     _swap_to_position(g, 0, idx2)
     r = A.apply_transpose(d1)
     st = GenState([d1], [l1], [], [np.array([r[g[0]]], dtype=np.float64)], t, g,
                   beta, alpha, 0, False, r0)
     st.last_solution_product = r.copy()
     st.sample_size, st.rng = sample_size, rng
+    st.storage = storage
     return st
 
 
@@ -361,7 +387,7 @@ def step_generalized(state, A, keep_products=True):
         return state
     h[k] = val
     _swap_to_position(state.t, k, idx)
-    d_new = u / val
+    d_new = _store(u / val, getattr(state, "storage", None))
     state.D.append(d_new)
     state.h_cols.append(h)
 
@@ -381,7 +407,7 @@ def step_generalized(state, A, keep_products=True):
         return state
     w[k] = val2
     _swap_to_position(state.g, k, idx2)
-    state.L.append(q / val2)
+    state.L.append(_store(q / val2, getattr(state, "storage", None)))
     state.w_cols.append(w)
     state.k = k
     return state
@@ -490,6 +516,7 @@ class Result:
 def hessenberg_solve(
     A, b, *, square, maxiter, ell=None, lam=0.0, seed=0, S2=None, S1=None,
     x0=None, x_true=None, sketch_basis=False, sketched=True, pivot_sample=0, pivot_seed=0, printed_f=False,
+    storage=None,
 ):
     """Restates ``_hessenberg_solve`` (solvers.py:410-539) for the sketched
     solvers ``scmrh`` / ``slslu`` / ``*_tikhonov`` (solvers.py:562-605) and,
@@ -512,7 +539,7 @@ def hessenberg_solve(
     init = init_square if square else init_generalized
     rng = np.random.default_rng(pivot_seed) if pivot_sample else None
     try:
-        state = init(A, b, x0=x0, sample_size=pivot_sample, rng=rng)
+        state = init(A, b, x0=x0, sample_size=pivot_sample, rng=rng, storage=storage)
     except TrivialSolution as sig:
         return Result(x=sig.x, records=[], termination="trivial")
     if not sketched:

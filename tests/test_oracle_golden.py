@@ -315,3 +315,30 @@ def test_gmres_lsqr_bitwise(golden):
     t = golden("slslu_tomo16")
     K = _csr(golden("tomo_matrices"), "tomo16x12_")
     _check_krylov(ho.lsqr(ho.csr_operator(K), t["b"], maxiter=30, x_true=t["x_true"], diagnostics=True), g, "ls_tomo_")
+
+
+def test_bf16_storage_oracle():
+    """oracle32 with bf16 basis storage (config 5's device path): the rounding
+    is round-to-nearest-even (torch's bfloat16 conversion), the stored basis is
+    bf16-representable with exact unit pivots and exact zeros at earlier pivot
+    rows, and H is the elimination on the stored columns."""
+    import torch
+
+    from oracle import hessketch_oracle as ho
+
+    rng = np.random.default_rng(0)
+    a = (rng.standard_normal(20000) * 10.0 ** rng.integers(-20, 20, 20000)).astype(np.float32)
+    assert np.array_equal(ho.round_bf16(a), torch.from_numpy(a).to(torch.bfloat16).float().numpy())
+    n, K = 200, 12
+    M = rng.standard_normal((n, n)).astype(np.float32)
+    A = ho.dense_operator(M, np.float32)
+    b = rng.standard_normal(n)
+    ref = ho.hessenberg_solve(A, b, square=True, maxiter=K, S2=rng.standard_normal((4 * K, n)), storage="bfloat16")
+    L = np.column_stack(ref.state.L)
+    assert np.array_equal(ho.round_bf16(L), L)
+    t, _ = ho.pivots_of(ref.state)
+    P = L[t[: L.shape[1]], :]
+    assert np.all(np.diag(P) == 1.0) and np.all(np.triu(P, 1) == 0.0)
+    # without bf16 storage the same problem keeps fp32 columns (not all bf16-representable)
+    ref32 = ho.hessenberg_solve(A, b, square=True, maxiter=K, S2=rng.standard_normal((4 * K, n)))
+    assert not np.array_equal(ho.round_bf16(np.column_stack(ref32.state.L)), np.column_stack(ref32.state.L))
