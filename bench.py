@@ -53,6 +53,19 @@ WORKLOADS = {
 }
 
 
+def workload_config(args, grid, angles, bins, nnz, K, ell, ws):
+    """The `config` object of both arms' JSON lines (identical for the same
+    workload and N; how each arm executes it goes into its own keys)."""
+    return {
+        "workload": f"cfg{args.config}: " + WORKLOADS[args.config],
+        "grid": grid, "angles": angles, "bins": bins, "nnz": nnz, "maxiter": K,
+        "sketch": "sparse-sign ell=%d zeta=8" % ell,
+        "step": "one full sLSLU solve (maxiter iterations)",
+        "l2": "inputs (A + A^T) far larger than L2; no flush",
+        "parallelism": f"rowshard{ws}" if ws > 1 else "single",
+    }
+
+
 def _traffic(args):
     """DRAM bytes per SpMV launch from the committed ncu capture (config 4 only)."""
     if args.config != 4 or args.scale:
@@ -145,6 +158,17 @@ def max_over_ranks(x, ws):
     return float(t.item())
 
 
+def gather_ranks(x, ws):
+    """Per-rank values (rank order) on every rank."""
+    if ws == 1:
+        return [x]
+    import torch.distributed as dist
+
+    out = [None] * ws
+    dist.all_gather_object(out, x)
+    return out
+
+
 def barrier(ws):
     if ws > 1:
         import torch.distributed as dist
@@ -201,6 +225,7 @@ def run_ours(args, ws, rank, local):
     stats = ctx.kernel_stats()
     clocks = clk.summary()
 
+    per_rank = gather_ranks(round(sum(loop_ms), 3), ws)
     tot_ms = max_over_ranks(sum(loop_ms), ws)
     tot_wall = max_over_ranks(sum(wall_s), ws)
     iters_all = iters  # one sharded solve across all ranks (strong scaling)
@@ -230,14 +255,12 @@ def run_ours(args, ws, rank, local):
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic (seeded random-ellipse phantom, 1% noise; device-built exact-chord operator)",
-        "config": {
-            "workload": f"cfg{args.config}: " + WORKLOADS[args.config],
-            "grid": w.meta.get("grid"), "angles": w.meta.get("angles"), "bins": w.meta.get("bins"),
-            "nnz": inf.get("nnz"), "maxiter": K, "sketch": "sparse-sign ell=%d zeta=8" % w.cfg.sketch_rows,
-            "step": "one full sLSLU solve (maxiter iterations)",
-            "l2": "inputs (A + A^T) far larger than L2; no flush",
-            "parallelism": f"rowshard{ws} (NCCL all-gathers + owner picks)" if ws > 1 else "single",
-        },
+        "config": workload_config(args, w.meta.get("grid"), w.meta.get("angles"), w.meta.get("bins"),
+                                  w.meta.get("nnz"), K, w.cfg.sketch_rows, ws),
+        "parallelism_detail": ("row-sharded operator and bases, NCCL all-gathers of l_k / d_{k+1} and of the "
+                               "sketch partials, owner-picked pivot rows, merged argmax candidates"
+                               if ws > 1 else "one GPU"),
+        "per_rank_loop_ms": per_rank,
         "e2e": {"value": round(e2e, 3), "unit": UNIT,
                 "h2d_bytes_per_step": int(w.b.nbytes + w.x_true.nbytes),
                 "d2h_bytes_per_step": int(w.x_true.nbytes + 8 * 12 * K)},
@@ -277,6 +300,20 @@ def cpu_baseline(args, w, seconds=None):
         return {"value": None, "unit": UNIT, "cores": None, "kind": "port", "sample": f"unavailable: {e}"}
 
 
+def _python_reference_note():
+    """The measured seconds per iteration of the unmodified Python reference at
+    a reduced size (tools/ref_python_scaled.py, run where /root/reference
+    exists; the committed measurement travels, the reference does not)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2", "reference_python_scaled.json")) as fh:
+            r = json.load(fh)
+        return {k: r[k] for k in ("grid", "angles", "bins", "nnz", "maxiter", "python_reference_s_per_iter",
+                                  "c_port_s_per_iter", "python_over_c_port",
+                                  "python_reference_full_size_estimate_s_per_iter", "host_threads")}
+    except Exception:
+        return None
+
+
 def run_reference(args, ws, rank):
     if rank != 0:
         return None
@@ -291,30 +328,31 @@ def run_reference(args, ws, rank):
         f = args.scale / grid
         grid, angles, bins = args.scale, max(2, round(angles * f)), max(2, round(bins * f))
     K = args.maxiter or K
+    ell = max(ell, K + 1)
     # host-only workload description (the operator, phantom and b are built on the host by oracle/)
     w = SimpleNamespace(meta={"grid": grid, "angles": angles, "bins": bins},
-                        cfg=SimpleNamespace(maxiter=K, sketch_rows=max(ell, K + 1)))
-    vals = []
-    last = None
+                        cfg=SimpleNamespace(maxiter=K, sketch_rows=ell))
+    vals, last = [], None
+    t_all = time.perf_counter()
     for i in range(args.warmup + args.steps):
-        r = cb.run(w, budget_s=args.cpu_seconds / 2)
+        r = cb.run(w, real_iters=4 if i == 0 else 0)
         if i >= args.warmup:
             vals.append(r["value"])
+        if last is None or i == 0:
+            first = r
         last = r
     value = statistics.mean(vals) if vals else None
+    sample = (first["sample"] + f"; {args.steps} timed steps (+{args.warmup} warm-up), each the same {K}-step "
+              f"profile: rate mean {value:.4f}, min {min(vals):.4f}, max {max(vals):.4f} it/s; "
+              f"{time.perf_counter() - t_all:.0f}s in all")
     return {
         "metric": METRIC, "impl": "reference", "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic",
-        # the same workload description as the device arm's line
-        "config": {"workload": f"cfg{args.config}: " + WORKLOADS[args.config], "grid": grid, "angles": angles,
-                   "bins": bins, "nnz": last.get("nnz") if last else None, "maxiter": K,
-                   "sketch": "sparse-sign ell=%d zeta=8" % w.cfg.sketch_rows,
-                   "step": "one full sLSLU solve (maxiter iterations; CPU: bounded sample, rate extrapolated)",
-                   "l2": "inputs (A + A^T) far larger than L2; no flush", "parallelism": "single (host threads)",
-                   "sample": last["sample"] if last else None},
+        "data": "synthetic (seeded random-ellipse phantom, 1% noise; host-built exact-chord operator)",
+        "config": workload_config(args, grid, angles, bins, last.get("nnz") if last else None, K, ell, ws),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": last["cores"] if last else None, "kind": "port",
-                         "sample": last["sample"] if last else None},
+                         "sample": sample},
+        "python_reference": _python_reference_note(),
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -332,7 +370,19 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: relaunch this command under torchrun
+        import socket
+
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        os.execv(sys.executable, cmd)
     ws, rank, local = dist_env()
+    if ws != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
     if ws > 1:
         import torch
         import torch.distributed as dist

@@ -544,3 +544,131 @@ out2:
   free(L); free(t); free(hcol); free(u);
   return done;
 }
+
+/* ---- reference-arm cost probe: one sLSLU iteration of co_slslu_f32 at step k ----
+   The loop's per-iteration work depends on k (k-pass eliminations on both
+   sides, the from-scratch QR of the l x k sketched matrix, the iterate
+   x = L_k y), not on the basis values, so the rate of a full K-iteration run is
+   the mean over k of one iteration's time at each k.  The probe holds a
+   K-column stand-in basis (pseudo-random fp32 columns, distinct pivot
+   positions) and times the body of co_slslu_f32's loop at any k without
+   running the k - 1 iterations before it. */
+typedef struct {
+  int64_t m, n, ell;
+  int kmax;
+  float **D, **L;
+  int64_t *t, *g;
+  double *Z, *sr0, *y, *work, *hcol, *x;
+  float *u, *q;
+} co_probe;
+
+static float prand(uint64_t* s) {
+  *s = *s * 6364136223846793005ULL + 1442695040888963407ULL;
+  return (float)((double)(*s >> 40) / (double)(1ULL << 24)) * 2.0f - 1.0f;
+}
+
+void* co_probe_create(int64_t m, int64_t n, int64_t ell, int kmax, int nthreads) {
+  const int T = nthreads > 0 ? nthreads : omp_get_max_threads();
+  co_probe* p = (co_probe*)calloc(1, sizeof(co_probe));
+  p->m = m; p->n = n; p->ell = ell; p->kmax = kmax;
+  p->D = (float**)calloc((size_t)kmax + 2, sizeof(float*));
+  p->L = (float**)calloc((size_t)kmax + 2, sizeof(float*));
+  p->t = (int64_t*)calloc((size_t)kmax + 2, sizeof(int64_t));
+  p->g = (int64_t*)calloc((size_t)kmax + 2, sizeof(int64_t));
+  for (int j = 0; j <= kmax; ++j) {
+    p->D[j] = (float*)malloc(sizeof(float) * (size_t)m);
+    p->L[j] = (float*)malloc(sizeof(float) * (size_t)n);
+    p->t[j] = (int64_t)(((uint64_t)j * 2654435761ULL) % (uint64_t)m);
+    p->g[j] = (int64_t)(((uint64_t)j * 40503ULL + 17) % (uint64_t)n);
+#pragma omp parallel num_threads(T)
+    {
+      uint64_t sd = 0x9E3779B97F4A7C15ULL ^ ((uint64_t)j << 20) ^ (uint64_t)omp_get_thread_num();
+#pragma omp for schedule(static)
+      for (int64_t i = 0; i < m; ++i) p->D[j][i] = prand(&sd);
+#pragma omp for schedule(static)
+      for (int64_t i = 0; i < n; ++i) p->L[j][i] = prand(&sd);
+    }
+  }
+  /* unit pivots, zeros at the other pivot rows (as partial pivoting leaves
+     them): the elimination coefficients stay the size of u's entries */
+  for (int j = 0; j <= kmax; ++j)
+    for (int i = 0; i <= kmax; ++i) {
+      p->D[j][p->t[i]] = i == j ? 1.0f : 0.0f;
+      p->L[j][p->g[i]] = i == j ? 1.0f : 0.0f;
+    }
+  p->Z = (double*)malloc(sizeof(double) * (size_t)ell * (kmax + 1));
+  uint64_t sd = 12345;
+  for (int64_t i = 0; i < ell * (kmax + 1); ++i) p->Z[i] = (double)prand(&sd);
+  p->sr0 = (double*)malloc(sizeof(double) * (size_t)ell);
+  for (int64_t i = 0; i < ell; ++i) p->sr0[i] = (double)prand(&sd);
+  p->y = (double*)calloc((size_t)kmax + 1, sizeof(double));
+  p->work = (double*)malloc(sizeof(double) * ((size_t)ell * (kmax + 1) + ell));
+  p->hcol = (double*)calloc((size_t)kmax + 2, sizeof(double));
+  p->x = (double*)malloc(sizeof(double) * (size_t)n);
+  p->u = (float*)malloc(sizeof(float) * (size_t)m);
+  p->q = (float*)malloc(sizeof(float) * (size_t)n);
+  return p;
+}
+
+void co_probe_destroy(void* vp) {
+  co_probe* p = (co_probe*)vp;
+  if (!p) return;
+  for (int j = 0; j <= p->kmax; ++j) {
+    free(p->D[j]);
+    free(p->L[j]);
+  }
+  free(p->D); free(p->L); free(p->t); free(p->g); free(p->Z); free(p->sr0); free(p->y); free(p->work);
+  free(p->hcol); free(p->x); free(p->u); free(p->q);
+  free(p);
+}
+
+/* seconds for one iteration of co_slslu_f32's loop body at step k (1 <= k <= kmax) */
+double co_probe_iter(void* vp, int k, const int64_t* Arp, const int32_t* Aci, const float* Acv, const int64_t* Trp,
+                     const int32_t* Tci, const float* Tcv, const int64_t* Srp, const int32_t* Sci, const double* Scv,
+                     int nthreads) {
+  co_probe* p = (co_probe*)vp;
+  const int T = nthreads > 0 ? nthreads : omp_get_max_threads();
+  const int64_t m = p->m, n = p->n, ell = p->ell;
+  int64_t idx;
+  float val;
+  const double tic = now_s();
+  spmv_f32(m, Arp, Aci, Acv, p->L[k - 1], p->u, T);
+  sketch_csr(ell, Srp, Sci, Scv, p->u, p->Z + (size_t)(k - 1) * ell, T);
+  eliminate(p->u, m, p->D, p->t, k, p->hcol, T);
+  argmax_abs(p->u, m, &idx, &val, T);
+  if (val == 0.0f) val = 1.0f;
+  {
+    float* dk = p->D[k];
+    const float* u = p->u;
+#pragma omp parallel for schedule(static) num_threads(T)
+    for (int64_t i = 0; i < m; ++i) dk[i] = u[i] / val;
+  }
+  spmv_f32(n, Trp, Tci, Tcv, p->D[k], p->q, T);
+  eliminate(p->q, n, p->L, p->g, k, p->hcol, T);
+  argmax_abs(p->q, n, &idx, &val, T);
+  if (val == 0.0f) val = 1.0f;
+  {
+    float* lk = p->L[k];
+    const float* q = p->q;
+#pragma omp parallel for schedule(static) num_threads(T)
+    for (int64_t i = 0; i < n; ++i) lk[i] = q[i] / val;
+  }
+  ls_qr(p->Z, ell, k, p->sr0, p->y, p->work);
+  double s2 = 0.0;
+  for (int64_t i = 0; i < ell; ++i) {
+    double a = -p->sr0[i];
+    for (int j = 0; j < k; ++j) a += p->Z[(size_t)j * ell + i] * p->y[j];
+    s2 += a * a;
+  }
+  p->hcol[0] = s2;
+  double* x = p->x;
+  const double* y = p->y;
+  float** L = p->L;
+#pragma omp parallel for schedule(static) num_threads(T)
+  for (int64_t e = 0; e < n; ++e) {
+    double a = 0.0;
+    for (int j = 0; j < k; ++j) a += y[j] * (double)L[j][e];
+    x[e] = a;
+  }
+  return now_s() - tic;
+}

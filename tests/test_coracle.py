@@ -40,8 +40,12 @@ def test_c_port_matches_oracle32():
     assert np.linalg.norm(r["x"] - ref.x) <= 1e-9 * np.linalg.norm(ref.x)
 
 
-def test_rate_extrapolation():
-    its = 0.1 + 0.01 * np.arange(1, 21)
-    rate, a, b = cb.extrapolate_rate(its, 300)
-    assert abs(a - 0.1) < 1e-9 and abs(b - 0.01) < 1e-9
-    assert abs(rate - 1.0 / (0.1 + 0.01 * 150.5)) < 1e-9
+def test_probe_rate_runs_every_step():
+    """The reference-arm cost probe times one loop-body iteration at steps
+    spread over k = 1..K and averages the interpolated t(k) over every k."""
+    grid, angles, bins, K, ell = 48, 30, 69, 40, 200
+    A, At, m, n = cb.host_tomography(grid, angles, bins, 4)
+    rate, ks, times = cb.probe_rate(A, At, m, n, ell, K, 4, kpoints=5)
+    assert ks[0] == 1 and ks[-1] == K and len(ks) == 5
+    assert all(t > 0 for t in times)
+    assert abs(1.0 / rate - np.mean(np.interp(np.arange(1, K + 1), ks, times))) < 1e-12
