@@ -106,6 +106,8 @@ int hs_ctx_kernel_names(hs_ctx* ctx, char* buf, int64_t cap);
 const char* hs_version(void);
 /* number of CUDA kernels this library has launched in this process */
 unsigned long long hs_launch_count(void);
+/* HS_GUARD=1: buffers released with a changed guard band (out-of-bounds writes) */
+unsigned long long hs_guard_violations(void);
 
 /* context: one CUDA device, one stream */
 int hs_ctx_create(int device, hs_ctx** out);

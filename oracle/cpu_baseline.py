@@ -181,3 +181,26 @@ def run(w, budget_s=20.0, nthreads=None, b=None, real_iters=4):
                    f"operator ({int(A[0][-1])} nnz, host-built in {build_s:.1f}s): one iteration timed at each of "
                    f"{len(ks)} steps ({pts}; {probe_s:.1f}s), mean over k=1..{K} by linear interpolation{chk}"),
     }
+
+
+def psf_conv(img, kernel, nthreads=None):
+    """Order-specified zero-boundary convolution (tomo_oracle.psf_stencil,
+    transpose=False) of a float32 image, in C."""
+    img = np.ascontiguousarray(img, dtype=np.float32)
+    K = np.ascontiguousarray(kernel, dtype=np.float32)
+    out = np.empty_like(img)
+    lib().co_psf_conv_f32(img.shape[0], img.shape[1], _p(K), K.shape[0], K.shape[1], _p(img), _p(out),
+                          nthreads or os.cpu_count())
+    return out
+
+
+def scmrh_psf_pivots(shape, kernel, b, maxiter, nthreads=None):
+    """The square Hessenberg process (hessenberg.py:160-226) on the PSF
+    operator with float32 vectors and basis, in C: (pivots t[:done+1], H)."""
+    K = np.ascontiguousarray(kernel, dtype=np.float32)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    t = np.zeros(maxiter + 1, dtype=np.int64)
+    h = np.zeros((maxiter, maxiter + 1))
+    done = lib().co_scmrh_psf_f32(shape[0], shape[1], _p(K), K.shape[0], K.shape[1], _p(b), maxiter,
+                                  nthreads or os.cpu_count(), _p(t), _p(h))
+    return t[: done + 1], np.ascontiguousarray(h[:done].T)

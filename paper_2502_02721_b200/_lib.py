@@ -53,6 +53,7 @@ _SIGNATURES = [
     ("hs_last_error", ctypes.c_char_p, []),
     ("hs_version", ctypes.c_char_p, []),
     ("hs_launch_count", ctypes.c_ulonglong, []),
+    ("hs_guard_violations", ctypes.c_ulonglong, []),
     ("hs_ctx_create", c_i32, [ctypes.c_int, ctypes.POINTER(c_vp)]),
     ("hs_ctx_destroy", c_i32, [c_vp]),
     ("hs_ctx_synchronize", c_i32, [c_vp]),

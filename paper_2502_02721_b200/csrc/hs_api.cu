@@ -116,11 +116,23 @@ struct StreamRef {
 };
 static thread_local std::shared_ptr<StreamRef> tl_alloc;
 
+// Guard mode (HS_GUARD=1, read at each allocation; compute-sanitizer is not
+// available on the GPU pool): every buffer gets 4 KB guard bands filled with
+// 0xA5 on both sides, checked when the buffer is released; a changed byte is
+// an out-of-bounds write by some kernel, counted in hs_guard_violations().
+constexpr size_t kGuard = 4096;
+static std::atomic<unsigned long long> g_guard_violations{0};
+static bool guard_mode() {
+  const char* e = getenv("HS_GUARD");
+  return e && *e && !(e[0] == '0' && e[1] == 0);
+}
+
 // device buffer with RAII
 struct DBuf {
   void* p = nullptr;
   size_t bytes = 0;
   std::shared_ptr<StreamRef> owner;
+  bool guarded = false;
   DBuf() = default;
   explicit DBuf(size_t b, bool zero = true) { alloc(b, zero); }
   void alloc(size_t b, bool zero = true) {
@@ -128,34 +140,67 @@ struct DBuf {
     bytes = b;
     if (b) {
       owner = tl_alloc;
+      guarded = guard_mode();
+      const size_t total = guarded ? b + 2 * kGuard : b;
+      void* base = nullptr;
       if (owner) {
-        CK(cudaMallocAsync(&p, b, owner->s));
-        if (zero) CK(cudaMemsetAsync(p, 0, b, owner->s));
-        // buffers are also filled by pageable-host copies and read by the
-        // context's second stream: make the allocation complete now
-        CK(cudaStreamSynchronize(owner->s));
+        CK(cudaMallocAsync(&base, total, owner->s));
       } else {
-        CK(cudaMalloc(&p, b));
-        if (zero) CK(cudaMemset(p, 0, b));
+        CK(cudaMalloc(&base, total));
       }
+      p = guarded ? reinterpret_cast<char*>(base) + kGuard : base;
+      cudaStream_t s = owner ? owner->s : nullptr;
+      if (zero) CK(cudaMemsetAsync(p, 0, b, s));
+      if (guarded) {
+        CK(cudaMemsetAsync(base, 0xA5, kGuard, s));
+        CK(cudaMemsetAsync(reinterpret_cast<char*>(p) + b, 0xA5, kGuard, s));
+      }
+      // buffers are also filled by pageable-host copies and read by the
+      // context's second stream: make the allocation complete now
+      CK(cudaStreamSynchronize(s));
+    }
+  }
+  void check_guards() {
+    cudaStream_t s = owner ? owner->s : nullptr;
+    std::vector<unsigned char> g(2 * kGuard);
+    if (cudaStreamSynchronize(s) != cudaSuccess ||
+        cudaMemcpy(g.data(), reinterpret_cast<char*>(p) - kGuard, kGuard, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(g.data() + kGuard, reinterpret_cast<char*>(p) + bytes, kGuard, cudaMemcpyDeviceToHost) !=
+            cudaSuccess)
+      return;
+    size_t bad = 0, first = 0;
+    for (size_t i = 0; i < g.size(); ++i)
+      if (g[i] != 0xA5 && bad++ == 0) first = i;
+    if (bad) {
+      ++g_guard_violations;
+      fprintf(stderr, "[hessketch guard] %zu bytes changed %s a %zu-byte buffer (first at guard offset %zu)\n", bad,
+              first < kGuard ? "before" : "after", bytes, first % kGuard);
     }
   }
   void release() {
     if (p) {
-      if (owner) cudaFreeAsync(p, owner->s);  // ordered after the owning stream's work
-      else cudaFree(p);
+      if (guarded) check_guards();
+      void* base = guarded ? reinterpret_cast<char*>(p) - kGuard : p;
+      if (owner) cudaFreeAsync(base, owner->s);  // ordered after the owning stream's work
+      else cudaFree(base);
     }
     p = nullptr;
     bytes = 0;
     owner.reset();
+    guarded = false;
   }
   ~DBuf() { release(); }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes), owner(std::move(o.owner)) { o.p = nullptr; o.bytes = 0; }
+  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes), owner(std::move(o.owner)), guarded(o.guarded) {
+    o.p = nullptr;
+    o.bytes = 0;
+    o.guarded = false;
+  }
   DBuf& operator=(DBuf&& o) noexcept {
     release();
-    p = o.p; bytes = o.bytes; owner = std::move(o.owner); o.p = nullptr; o.bytes = 0;
+    p = o.p; bytes = o.bytes; owner = std::move(o.owner); guarded = o.guarded;
+    o.p = nullptr; o.bytes = 0; o.guarded = false;
     return *this;
   }
   template <class T> T* as() const { return reinterpret_cast<T*>(p); }
@@ -2016,6 +2061,7 @@ extern "C" {
 
 const char* hs_last_error(void) { return g_err.c_str(); }
 unsigned long long hs_launch_count(void) { return g_launches; }
+unsigned long long hs_guard_violations(void) { return g_guard_violations; }
 const char* hs_version(void) { return "hessketch_b200 0.1.0 (sm_100a)"; }
 
 int hs_ctx_create(int device, hs_ctx** out) {

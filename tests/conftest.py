@@ -22,3 +22,14 @@ def golden():
         with np.load(os.path.join(GOLDEN, name + ".npz"), allow_pickle=False) as z:
             return {k: z[k] for k in z.files}
     return load
+
+
+@pytest.fixture(autouse=True)
+def _release_device_objects():
+    """Full-size tests hold tens of GB of device operators; Python reference
+    cycles (result <-> factorization) can keep them past the test unless the
+    cycle collector runs, so collect after every test."""
+    yield
+    import gc
+
+    gc.collect()

@@ -49,3 +49,30 @@ def test_probe_rate_runs_every_step():
     assert ks[0] == 1 and ks[-1] == K and len(ks) == 5
     assert all(t > 0 for t in times)
     assert abs(1.0 / rate - np.mean(np.interp(np.arange(1, K + 1), ks, times))) < 1e-12
+
+
+def test_c_psf_conv_matches_oracle_stencil():
+    """The C stencil used for the full-size config-5 pivot check is the
+    oracle's order-specified convolution, bit for bit."""
+    from paper_2502_02721_b200.problems import gaussian_psf
+
+    img = np.random.default_rng(1).standard_normal((45, 38)).astype(np.float32)
+    for r in (3, 7, 15):
+        psf = gaussian_psf(2.0, radius=r)
+        np.testing.assert_array_equal(cb.psf_conv(img, psf, 4), to.psf_stencil(img, psf, False, np.float32))
+
+
+def test_c_scmrh_pivots_match_oracle32():
+    from paper_2502_02721_b200.problems import gaussian_psf
+
+    rng = np.random.default_rng(2)
+    H, W, K = 40, 36, 25
+    psf = gaussian_psf(2.0, radius=7)
+    b = rng.standard_normal(H * W)
+    t, Hc = cb.scmrh_psf_pivots((H, W), psf, b, K, 4)
+    A = ho.Operator(H * W, H * W, lambda v: to.psf_stencil(v.reshape(H, W), psf, False, np.float32).ravel(),
+                    lambda v: to.psf_stencil(v.reshape(H, W), psf, True, np.float32).ravel(), np.float32)
+    ref = ho.hessenberg_solve(A, b, square=True, maxiter=K, S2=rng.standard_normal((4 * K, H * W)))
+    t_ref, _ = ho.pivots_of(ref.state)
+    np.testing.assert_array_equal(t, t_ref)
+    np.testing.assert_array_equal(Hc, ref.state.H_matrix())
