@@ -625,6 +625,16 @@ struct hs_op {
     return yB.p;
   }
 
+  // tomography A input staged by the caller in the transposed image layout
+  // (the loop's L-side normalisation writes it beside l_{k+1}); null if the
+  // operator has no transposed-layout slices
+  void* transposed_input(size_t elem_bytes) const {
+    if (kind != OP_CSR || sflag.p == nullptr || img_grid <= 0 || As.nslices <= 0 || sharded) return nullptr;
+    const size_t need = (size_t)n * elem_bytes;
+    if (xT.bytes < need) xT.alloc(need, false);
+    return xT.p;
+  }
+
   template <class V, class Tin, class T>
   void apply_t(const void* x, void* y, bool transpose, bool preblocked = false) const {
     cudaStream_t s = ctx->stream;
@@ -650,7 +660,9 @@ struct hs_op {
         CKL();
         xi = yB.as<Tin>();
       }
-      if (tflag) {
+      if (tflag && preblocked) {
+        // the caller wrote the transposed image copy beside x (normalize_transpose_kernel)
+      } else if (tflag) {
         // transposed image copy of x for the near-horizontal ray slices
         Prof p(ctx, "x_transpose", 2.0 * (double)n * sizeof(Tin));
         const size_t need = (size_t)n * sizeof(Tin);
@@ -1710,6 +1722,13 @@ struct Solver {
     for (int i = 0; i <= K; ++i) hflag[i] = 0;
     flag_ev = ctx->take_events(K + 1, false);
 
+    // rectangular tomography: the L-side normalisation also writes the
+    // transposed image copy the next A apply gathers from (not with the
+    // diagnostics, whose extra forward applies reuse the operator's copy)
+    B* const lT = (!square && !diag && !env_flag("HS_NO_XT_FUSE"))
+                      ? reinterpret_cast<B*>(op->transposed_input(sizeof(B)))
+                      : nullptr;
+    bool lT_ready = false;
     CK(cudaEventRecord(ev[0], s));
     int k_last = 0;
     int bd_at = 0;
@@ -1733,7 +1752,7 @@ struct Solver {
         // u is free once the previous iteration's sketch has read it
         CK(cudaStreamWaitEvent(s, ev_sk, 0));
       }
-      op->apply(Lcol(k - 1), bdt, ucur, wdt, false);
+      op->apply(Lcol(k - 1), bdt, ucur, wdt, false, lT_ready);
       if (diag_eps) qW.append(u.as<T>());  // the unreduced A l_k (solvers.py:480-481)
       // rectangular: the sketch of u (and the projected solve after it) starts
       // once the data side is normalised, so the aux stream overlaps the long
@@ -1802,8 +1821,16 @@ struct Solver {
                                                     n, st, 1, k, pv.as<T>() + 1);
         CKL();
         swap_perm(1, k);
-        normalize_kernel<T, B><<<grid_for(ldn, 256, NORM_G), 256, 0, s>>>(n, ldn, q.as<T>(), pv.as<T>() + 1, Lcol(k), st, 1, k);
+        if (lT) {
+          const dim3 tg((op->img_grid + 31) / 32, (op->img_grid + 31) / 32);
+          normalize_transpose_kernel<T, B><<<tg, 256, 0, s>>>(op->img_grid, ldn, q.as<T>(), pv.as<T>() + 1, Lcol(k),
+                                                              lT, st, k);
+        } else {
+          normalize_kernel<T, B><<<grid_for(ldn, 256, NORM_G), 256, 0, s>>>(n, ldn, q.as<T>(), pv.as<T>() + 1, Lcol(k),
+                                                                            st, 1, k);
+        }
         CKL();
+        lT_ready = lT != nullptr;
       } else {
         if (skd && !ovl && !sb) S2->apply(u.p, wdt, Zb.as<double>() + (long long)(k - 1) * ell, skM, G2);
         fsub(ucur, tpos.as<long long>(), PL.as<T>(), ldp, k, k, 0, cvec.as<T>(), Hcol(k - 1));

@@ -412,6 +412,40 @@ normalize_kernel(long long n, long long n_pad, const T* __restrict__ u, const T*
   }
 }
 
+// The same normalisation for a grid x grid image vector (tomography L side),
+// also writing the transposed image dstT[c * grid + r] = dst[r * grid + c]:
+// the gather layout the next A apply's near-horizontal ray slices read
+// (hs_ops.cuh: image_transpose_kernel), formed here through a shared-memory
+// tile instead of a separate pass over the new basis column.
+template <class T, class B>
+__global__ void __launch_bounds__(256)
+normalize_transpose_kernel(int grid, long long n_pad, const T* __restrict__ u, const T* __restrict__ pivval,
+                           B* __restrict__ dst, B* __restrict__ dstT, const LoopState* __restrict__ st, int iter) {
+  if (st->bd_iter != 0 && st->bd_iter <= iter) return;
+  __shared__ B tile[32][33];
+  const T p = *pivval;
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int r = ty; r < 32; r += 8) {
+    const int gy = by + r, gx = bx + tx;
+    if (gy < grid && gx < grid) {
+      const long long e = (long long)gy * grid + gx;
+      const B v = cvt<B>(Rn<T>::div(u[e], p));
+      dst[e] = v;
+      tile[r][tx] = v;
+    }
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int gx = bx + r, gy = by + tx;
+    if (gx < grid && gy < grid) dstT[(long long)gx * grid + gy] = tile[tx][r];
+  }
+  if (blockIdx.x == 0 && blockIdx.y == 0) {  // zero padding [n, n_pad)
+    const long long n = (long long)grid * grid;
+    for (long long e = n + threadIdx.x; e < n_pad; e += blockDim.x) dst[e] = cvt<B>(T(0));
+  }
+}
+
 // plain argmax over a vector (init pivots of r0 / A^T r0); result into st->piv_*[side]
 template <class T>
 __global__ void __launch_bounds__(256)

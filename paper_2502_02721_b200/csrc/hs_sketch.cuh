@@ -302,10 +302,11 @@ __global__ void sparse_sign_gen_kernel(long long m, int ell, int zeta, uint2 key
 template <class Tin> struct SkStage { using T = float; };   // staged tile type (bf16, fp32: exact in fp32)
 template <> struct SkStage<double> { using T = double; };
 
-// grid (local tile slots, slice groups of 8); warp w of block (b, y) adds
-// slice 8 y + w of tile b
+// grid = local tile slots, SK_THREADS threads: one CTA per tile (the tile of
+// v is staged once), warp w adds slices w, w + SK_WARPS, ...
+constexpr int SK_THREADS = 768, SK_WARPS = SK_THREADS / 32;
 template <class Tin, int CB>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(SK_THREADS, 2)
 sketch_sparse_gather_kernel(int ell, int nsl, TileMap tm, long long col_offset, const long long* __restrict__ tbase,
                             const int* __restrict__ soff, const unsigned short* __restrict__ perm,
                             const unsigned short* __restrict__ ent, const Tin* __restrict__ v,
@@ -319,49 +320,59 @@ sketch_sparse_gather_kernel(int ell, int nsl, TileMap tm, long long col_offset, 
   const long long k = (col_offset + c0) / tm.tc;  // absolute tile
   const int n = (int)(c1 - c0), tc = (int)tm.tc;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int sl = blockIdx.y * 8 + warp;
-  const bool active = sl < nsl;
-  // this warp's slice bounds and output rows, fetched before the staging
   const int* so = soff + k * (nsl + 1);
-  const int a = active ? so[sl] : 0, L8 = active ? (so[sl + 1] - a) >> 8 : 0;
-  const unsigned r = active ? perm[(k * nsl + sl) * 32 + lane] : 0xFFFFu;
-  const uint4* ep = reinterpret_cast<const uint4*>(ent + tbase[k] + a) + lane;
+  const unsigned short* et = ent + tbase[k];
+  // this warp's first slice: bounds and output row fetched before the staging
+  int sl = warp;
+  int a = sl < nsl ? so[sl] : 0, b = sl < nsl ? so[sl + 1] : 0;
+  unsigned r = sl < nsl ? perm[(k * nsl + sl) * 32 + lane] : 0xFFFFu;
   // stage the tile: all of a thread's loads issued before any store
-  for (int i0 = 0; i0 <= tc; i0 += 16 * 256) {
+  for (int i0 = 0; i0 <= tc; i0 += 16 * SK_THREADS) {
     S t[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
-      const int i = i0 + u * 256 + (int)threadIdx.x;
+      const int i = i0 + u * SK_THREADS + (int)threadIdx.x;
       t[u] = i < n ? cvt<S>(__ldcs(v + c0 + i)) : S(0);
     }
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
-      const int i = i0 + u * 256 + (int)threadIdx.x;
+      const int i = i0 + u * SK_THREADS + (int)threadIdx.x;
       if (i <= tc) vs[i] = t[u];
     }
   }
   __syncthreads();
-  if (!active) return;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
   const unsigned pad = (unsigned)tc | ((unsigned)tc << 16);
-  for (int q0 = 0; q0 < L8; q0 += CB) {
-    uint4 w[CB];
+  while (sl < nsl) {
+    const int L8 = (b - a) >> 8;
+    const uint4* ep = reinterpret_cast<const uint4*>(et + a) + lane;
+    // the next slice's bounds and row, in flight during this one
+    const int sn = sl + SK_WARPS;
+    const int an = sn < nsl ? so[sn] : 0, bn = sn < nsl ? so[sn + 1] : 0;
+    const unsigned rn = sn < nsl ? perm[(k * nsl + sn) * 32 + lane] : 0xFFFFu;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int q0 = 0; q0 < L8; q0 += CB) {
+      uint4 w[CB];
 #pragma unroll
-    for (int q = 0; q < CB; ++q)
-      w[q] = q0 + q < L8 ? __ldcs(ep + (long long)(q0 + q) * 32) : make_uint4(pad, pad, pad, pad);
+      for (int q = 0; q < CB; ++q)
+        w[q] = q0 + q < L8 ? __ldcs(ep + (long long)(q0 + q) * 32) : make_uint4(pad, pad, pad, pad);
 #pragma unroll
-    for (int q = 0; q < CB; ++q) {
-      const unsigned u4[4] = {w[q].x, w[q].y, w[q].z, w[q].w};
+      for (int q = 0; q < CB; ++q) {
+        const unsigned u4[4] = {w[q].x, w[q].y, w[q].z, w[q].w};
 #pragma unroll
-      for (int h = 0; h < 8; ++h) {
-        const unsigned e = (u4[h >> 1] >> ((h & 1) * 16)) & 0xFFFFu;
-        const double x = (double)vs[e & 0x3FFFu];
-        const long long sg = (long long)(e & 0x8000u) << 48;  // sign bit -> bit 63
-        acc[h & 3] += __longlong_as_double(__double_as_longlong(x) ^ sg);
+        for (int h = 0; h < 8; ++h) {
+          const unsigned e = (u4[h >> 1] >> ((h & 1) * 16)) & 0xFFFFu;
+          const double x = (double)vs[e & 0x3FFFu];
+          const long long sg = (long long)(e & 0x8000u) << 48;  // sign bit -> bit 63
+          acc[h & 3] += __longlong_as_double(__double_as_longlong(x) ^ sg);
+        }
       }
     }
+    if (r != 0xFFFFu) part[(long long)blockIdx.x * ell + r] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    sl = sn;
+    a = an;
+    b = bn;
+    r = rn;
   }
-  if (r != 0xFFFFu) part[(long long)blockIdx.x * ell + r] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
 template <class Tin>
@@ -374,8 +385,7 @@ inline void sparse_partials(cudaStream_t s, int ell, TileMap tm, long long col_o
   const size_t smem = (size_t)(tm.tc + 1) * sizeof(typename SkStage<Tin>::T);
   auto kern = sketch_sparse_gather_kernel<Tin, 8>;
   ensure_smem((const void*)kern, smem);
-  kern<<<dim3((unsigned)nt, (unsigned)((nsl + 7) / 8)), 256, smem, s>>>(ell, nsl, tm, col_offset, tbase, soff, perm,
-                                                                       ent, v, part);
+  kern<<<(unsigned)nt, SK_THREADS, smem, s>>>(ell, nsl, tm, col_offset, tbase, soff, perm, ent, v, part);
 }
 
 // ---- general explicit sparse S (CSR by sketch rows, fp64 values) ------------

@@ -247,12 +247,39 @@ def _opt(v):
     return None if np.isnan(v) else v
 
 
+# Default sketches realised on the device, reused across solves with the same
+# (kind, shape, seed, context): the reference draws S again on every call
+# (solvers.py:452-459) with the same bits, so a repeated solve may reuse the
+# uploaded matrix.  The PCG64 draw is host work (~5 ms for config 1's 400 x 1024)
+# that would otherwise dominate a short solve's end-to-end time.  Bounded: a
+# few entries of at most 256 MB of device memory each.
+_SKETCH_CACHE = {}
+_SKETCH_CACHE_MAX, _SKETCH_CACHE_BYTES = 4, 256 << 20
+
+
 def _default_sketch(cfg, ell, in_rows, seed):
+    from . import _lib
+
+    ctx = _lib.context()
+    # only sketches of the process-wide contexts are kept (in-process rank
+    # contexts are closed by their owner)
+    cacheable = _lib._ctx.get(ctx.device) is ctx
+    key = (cfg.sketch_kind, int(ell), int(in_rows), int(seed), cfg.sketch_zeta, ctx.device)
+    hit = _SKETCH_CACHE.get(key) if cacheable else None
+    if hit is not None:
+        return hit
     if cfg.sketch_kind == "pcg64":
-        return device_sketch(make_gaussian_sketch(ell, in_rows, seed))
-    if cfg.sketch_kind == "gaussian":
-        return GaussianSketch(ell, in_rows, seed)
-    return SparseSignSketch(ell, in_rows, seed, cfg.sketch_zeta)
+        sk = device_sketch(make_gaussian_sketch(ell, in_rows, seed))
+    elif cfg.sketch_kind == "gaussian":
+        sk = GaussianSketch(ell, in_rows, seed)
+    else:
+        sk = SparseSignSketch(ell, in_rows, seed, cfg.sketch_zeta)
+    nbytes = {"pcg64": 8 * ell * in_rows, "sparse_sign": 3 * in_rows * cfg.sketch_zeta}.get(cfg.sketch_kind, 0)
+    if cacheable and nbytes <= _SKETCH_CACHE_BYTES:
+        if len(_SKETCH_CACHE) >= _SKETCH_CACHE_MAX:
+            _SKETCH_CACHE.pop(next(iter(_SKETCH_CACHE)))
+        _SKETCH_CACHE[key] = sk
+    return sk
 
 
 def pivot_positions(strategy, maxiter, rows, cols, square):

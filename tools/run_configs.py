@@ -30,11 +30,19 @@ for cid in ids:
     wall = time.perf_counter() - t1
     stats = ctx.kernel_stats()
     ctx.set_profiling(False)
+    # the same solve without the per-kernel event brackets
+    t2 = time.perf_counter()
+    rn = solve(w.operator, w.b, w.cfg, x_true=w.x_true, sketch=w.sketch)
+    wall_np = time.perf_counter() - t2
+    loop_np = rn.loop_ms
+    del rn
     rel = r.trace.column("rel_err")
     out = {
         "config": cid, "desc": CONFIGS[cid], "iters": len(r.trace.records), "termination": r.termination,
         "loop_ms": round(r.loop_ms, 2), "it_per_s": round(len(r.trace.records) / (r.loop_ms / 1e3), 1),
         "e2e_it_per_s": round(len(r.trace.records) / wall, 1), "setup_s": round(setup, 2),
+        "it_per_s_noprof": round(len(r.trace.records) / (loop_np / 1e3), 1),
+        "e2e_it_per_s_noprof": round(len(r.trace.records) / wall_np, 1),
         "rel_err_first_min_last": [round(rel[0], 5), round(min(rel), 5), round(rel[-1], 5)],
         "sres_last": r.trace.final().sres_norm, "rank_fallback": any(r.trace.column("rank_fallback")),
         "kernels_ms": {k: round(v["ms"], 2) for k, v in sorted(stats.items(), key=lambda kv: -kv[1]["ms"])},
