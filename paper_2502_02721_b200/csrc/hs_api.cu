@@ -598,8 +598,16 @@ struct hs_op {
   // padded block sizes m_blk / n_blk (the all-gathered vectors are P*blk long)
   bool sharded = false;
   long long m_off = 0, m_loc = 0, m_blk = 0, n_off = 0, n_loc = 0, n_blk = 0;
-  // tomography (hs_op_tomo_create): image side
+  // tomography (hs_op_tomo_create): image side, ray tables, and the slices
+  // of As whose columns RayGen regenerates (hs_ops.cuh: sell_spmv_imp_kernel)
   long long tomo_grid = 0;
+  int tomo_bins = 0;
+  DBuf tcos, tsin, toff, imp;
+  long long imp_slices = 0, imp_slots = 0;
+  RayTab ray_tab() const {
+    return RayTab{tcos.as<double>(), tsin.as<double>(), toff.as<double>(), tomo_bins, (int)tomo_grid,
+                  sharded ? m_off : 0};
+  }
   // tomography: per-slice transposed-layout flags of As and the scratch copy of x
   int img_grid = 0;
   DBuf sflag;
@@ -645,7 +653,10 @@ struct hs_op {
       const int grid = grid_for(M.nslices, 8, ctx->num_sms * 16);
       // algorithmic bytes of the stored encoding: values + column indices (4 B, or 2 B deltas)
       // + row lengths (+ row bases) + slice pointers + x once + y
-      const double bytes = (double)M.stored_values() * sizeof(V) + (double)M.nnz * M.index_bytes() +
+      const bool impl = !transpose && imp_slices > 0 && M.d16 && !M.d16v && !M.c8;
+      const double bytes = (double)M.stored_values() * sizeof(V) +
+                           ((double)M.nnz - (impl ? (double)imp_slots * M.nnz / std::max<long long>(M.slots, 1) : 0.0)) *
+                               M.index_bytes() +
                            (double)M.rows * M.slot_bytes() +
                            (double)M.n_exc * 4 + (double)M.nslices * 8 + (double)M.cols * sizeof(Tin) +
                            (double)M.rows * sizeof(T);
@@ -699,6 +710,22 @@ struct hs_op {
         } else {
           fail(HS_ERR_RUNTIME, "d16v SELL with non-fp32 values");
         }
+      } else if (impl) {
+        // implicit columns on the verified ray slices (RayGen), 16-bit deltas elsewhere
+        int gshift = -1;
+        if (img_grid > 0 && (img_grid & (img_grid - 1)) == 0) gshift = __builtin_ctz((unsigned)img_grid);
+        const bool p2 = gshift >= 0 || !tflag;
+        // resident blocks per SM: 6 caps registers at 40 (RayGen state spills to the stack), 4 allows 64
+        constexpr bool F32 = sizeof(T) == 4 && sizeof(V) == 4;
+        const bool b6 = F32 && env_flag("HS_IMP_MINB6");
+        auto kern = b6 ? (p2 ? sell_spmv_imp_kernel<V, Tin, T, true, F32 ? 6 : 3>
+                             : sell_spmv_imp_kernel<V, Tin, T, false, F32 ? 6 : 3>)
+                       : (p2 ? sell_spmv_imp_kernel<V, Tin, T, true, F32 ? 4 : 2>
+                             : sell_spmv_imp_kernel<V, Tin, T, false, F32 ? 4 : 2>);
+        kern<<<grid, 256, 0, s>>>(M.rows, M.nslices, M.sptr.as<long long>(), M.rlen.as<int>(), M.rbase.as<int>(),
+                                  M.dcol.as<short>(), M.val.as<V>(), xi, tflag ? xT.as<Tin>() : nullptr,
+                                  tflag ? sflag.as<unsigned char>() : nullptr, imp.as<unsigned char>(), ray_tab(),
+                                  gshift >= 0 ? gshift : 0, M.sorder.as<int>(), M.sched.as<unsigned int>(), yo);
       } else if (M.d16) {
         int gshift = -1;
         if (img_grid > 0 && (img_grid & (img_grid - 1)) == 0) gshift = __builtin_ctz((unsigned)img_grid);
@@ -898,6 +925,44 @@ struct hs_op {
 
   long long nnz_total() const { return kind == OP_CSR ? A.nnz : (kind == OP_DENSE ? m * n : 0); }
 };
+
+// Mark the slices of a tomography A (SELL copy with int32 columns, natural
+// row order) whose every row RayGen reproduces exactly; those slices then
+// stream values only (hs_ops.cuh: sell_spmv_imp_kernel).  Opt-in
+// (HS_IMPLICIT=1): bit-identical, and 4 instead of 6 B per nonzero, but the
+// per-image-row fp64 range update runs in divergent lanes almost every entry
+// for steep rays; config 4's A apply measured 10.7 ms against 3.6 ms for the
+// 16-bit deltas.
+static void tomo_enable_implicit(hs_ctx* ctx, hs_op* op) {
+  Sell& S = op->As;
+  if (S.nslices == 0 || S.col.p == nullptr || S.rperm.p != nullptr || !env_flag("HS_IMPLICIT")) return;
+  cudaStream_t s = ctx->stream;
+  DBuf bad(S.nslices, true);
+  tomo_implicit_check_kernel<<<grid_for(S.nslots(), 128, 1 << 30), 128, 0, s>>>(
+      S.rows, S.nslices, S.sptr.as<long long>(), S.rlen.as<int>(), S.col.as<int>(), op->ray_tab(),
+      bad.as<unsigned char>());
+  CKL();
+  std::vector<unsigned char> hb(S.nslices);
+  std::vector<long long> hp(S.nslices + 1);
+  CK(cudaMemcpyAsync(hb.data(), bad.p, S.nslices, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hp.data(), S.sptr.p, (S.nslices + 1) * sizeof(long long), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  std::vector<unsigned char> ok(S.nslices);
+  long long ns = 0, nslot = 0;
+  for (long long i = 0; i < S.nslices; ++i) {
+    ok[i] = hb[i] ? 0 : 1;
+    if (ok[i]) {
+      ++ns;
+      nslot += hp[i + 1] - hp[i];
+    }
+  }
+  if (ns == 0) return;
+  op->imp.alloc(S.nslices, false);
+  CK(cudaMemcpyAsync(op->imp.p, ok.data(), S.nslices, cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  op->imp_slices = ns;
+  op->imp_slots = nslot;
+}
 
 // build the transpose of a row-sorted CSR (rows x cols) on device: output rows
 // are the columns [cb, ce), each sorted by the original row index

@@ -764,6 +764,216 @@ __device__ __forceinline__ T d16_row_u2(const short* __restrict__ dp, const V* _
   return acc;
 }
 
+// ---- implicit column indices for the rays of a tomography A ---------------------
+// A row of A is a parallel-beam ray; its stored columns (sorted, canonical
+// CSR) are the pixels the ray crosses, image row by image row.  In image row
+// ry the ray covers the x-interval [xl, xh] (the band ry <= y <= ry + 1,
+// clipped to the image), so its pixels are floor(xl + eps) .. ceil(xh - eps) - 1
+// (eps = 1e-9 drops corner touches, as the builder's 1e-12 length gate does).
+// RayGen walks that sequence with a few fp64 operations per image row, so the
+// SpMV streams only the values: 4 B per nonzero instead of 6.  The rule is
+// not the builder's arithmetic, so it is checked against the stored columns of
+// every row at build time (tomo_implicit_check_kernel) and a slice uses it only
+// if all 32 of its rows match exactly (rays through grid corners, e.g. every
+// ray of the 90-degree angle, keep their stored 16-bit deltas).  Entry order,
+// products and adds are unchanged: bit-identical.
+struct RayTab {
+  const double* cos_t;
+  const double* sin_t;
+  const double* offsets;
+  int n_bins, grid;
+  long long row_offset;  // global ray index of local row 0 (row-sharded A)
+};
+
+constexpr double kRayEps = 1e-9;
+
+struct RayGen {
+  double ox, oy, mslope, y0, y1;
+  int ry, ry_end, cx, hi, grid, mode;  // mode 0: general, 1: one image row, 2: one image column
+  __device__ __forceinline__ bool row_range(int r) {
+    // explicit roundings (no contraction choices left to the compiler), so
+    // the build-time check and the SpMV see the same columns
+    const double ylo = fmax((double)r, y0), yhi = fmin((double)(r + 1), y1);
+    const double xa = fma(__dsub_rn(ylo, oy), mslope, ox), xb = fma(__dsub_rn(yhi, oy), mslope, ox);
+    const double xl = fmax(0.0, fmin(xa, xb)), xh = fmin((double)grid, fmax(xa, xb));
+    if (!(xh > xl)) return false;
+    cx = (int)floor(__dadd_rn(xl, kRayEps));
+    hi = (int)ceil(__dsub_rn(xh, kRayEps)) - 1;
+    return hi >= cx;
+  }
+  // the first image row with pixels at or after r (ry = ry_end + 1 when none)
+  __device__ __forceinline__ void seek(int r) {
+    ry = r;
+    if (mode == 0) {
+      while (ry <= ry_end && !row_range(ry)) ++ry;
+    } else if (mode == 1) {
+      cx = 0;
+      hi = grid - 1;
+    } else {
+      cx = hi = (int)floor(ox);
+    }
+  }
+  __device__ __forceinline__ void init(const RayTab& tb, long long row) {
+    const long long r = row + tb.row_offset;
+    const int a = (int)(r / tb.n_bins), j = (int)(r - (long long)a * tb.n_bins);
+    grid = tb.grid;
+    const double ct = tb.cos_t[a], st = tb.sin_t[a], s = tb.offsets[j];
+    const double half = (double)grid / 2.0;
+    ox = __dadd_rn(half, __dmul_rn(s, -st));
+    oy = __dadd_rn(half, __dmul_rn(s, ct));
+    ry = 0;
+    ry_end = -1;
+    mode = 0;
+    mslope = y0 = y1 = 0.0;
+    if (fabs(st) < 1e-12) {  // horizontal ray: one image row
+      if (oy > 0.0 && oy < (double)grid) { mode = 1; ry = ry_end = (int)floor(oy); }
+    } else if (fabs(ct) < 1e-12) {  // vertical ray: one image column
+      if (ox > 0.0 && ox < (double)grid) { mode = 2; ry = 0; ry_end = grid - 1; }
+    } else {
+      mslope = __ddiv_rn(ct, st);
+      const double ya = __dadd_rn(oy, __ddiv_rn(__dsub_rn(0.0, ox), mslope));
+      const double yb = __dadd_rn(oy, __ddiv_rn(__dsub_rn((double)grid, ox), mslope));
+      y0 = fmax(0.0, fmin(ya, yb));
+      y1 = fmin((double)grid, fmax(ya, yb));
+      if (y1 > y0) {
+        ry = (int)floor(__dadd_rn(y0, kRayEps));
+        ry_end = (int)ceil(__dsub_rn(y1, kRayEps)) - 1;
+      }
+    }
+    seek(ry);
+  }
+  __device__ __forceinline__ bool done() const { return ry > ry_end; }
+  // the current column, then advance
+  __device__ __forceinline__ int next() {
+    const int c = ry * grid + cx;
+    if (cx < hi) ++cx;
+    else seek(ry + 1);
+    return c;
+  }
+};
+
+// build-time check: bad[s] != 0 when any row of slice s differs from RayGen
+// (one thread per slot; rows in natural order: A has no slot permutation)
+__global__ void tomo_implicit_check_kernel(long long rows, long long nslices, const long long* __restrict__ sptr,
+                                           const int* __restrict__ rlen, const int* __restrict__ col, RayTab tb,
+                                           unsigned char* __restrict__ bad) {
+  const long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= nslices * 32) return;
+  const long long sl = slot >> 5;
+  const int lane = (int)(slot & 31);
+  const int len = rlen[slot];
+  bool ok = true;
+  if (slot < rows) {
+    RayGen g;
+    g.init(tb, slot);
+    const long long base = sptr[sl];
+    for (int e = 0; e < len && ok; ++e) {
+      if (g.done()) { ok = false; break; }
+      ok = g.next() == col[base + (long long)(e >> 2) * 128 + lane * 4 + (e & 3)];
+    }
+    ok = ok && g.done();
+  } else {
+    ok = len == 0;
+  }
+  if (!ok) bad[sl] = 1;
+}
+
+template <int GM, class V, class Tin, class T>
+__device__ __forceinline__ void imp_chunk(T& acc, RayGen& rg, const Chunk4<V>& v, const Tin* __restrict__ x, int m,
+                                          int sh, int grid) {
+  const int c0 = rg.next(), c1 = rg.next(), c2 = rg.next(), c3 = rg.next();
+  const T x0 = gather_x<T>(x, gpos<GM>(c0, m, sh, grid));
+  const T x1 = gather_x<T>(x, gpos<GM>(c1, m, sh, grid));
+  const T x2 = gather_x<T>(x, gpos<GM>(c2, m, sh, grid));
+  const T x3 = gather_x<T>(x, gpos<GM>(c3, m, sh, grid));
+  acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[0]), x0));
+  acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[1]), x1));
+  acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[2]), x2));
+  acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[3]), x3));
+}
+
+// one lane's row with implicit columns (the value stream only; the d16_row_u2 schedule)
+template <int GM, class V, class Tin, class T>
+__device__ __forceinline__ T imp_row(const V* __restrict__ vp, RayGen rg, int len, const Tin* __restrict__ x, int m,
+                                     int sh, int grid) {
+  T acc = T(0);
+  const int nq = (len + 3) >> 2, nfull = len >> 2;
+  if (nq == 0) return acc;
+  Chunk4<V> v = Chunk4<V>::load(vp);
+#pragma unroll 2
+  for (int q = 0; q < nfull; ++q) {
+    const long long qn = min(q + 1, nq - 1);
+    const Chunk4<V> vn = Chunk4<V>::load(vp + qn * 128);
+    imp_chunk<GM>(acc, rg, v, x, m, sh, grid);
+    v = vn;
+  }
+  const int rem = len & 3;
+  if (rem) {
+    const int c0 = rg.next();
+    acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[0]), gather_x<T>(x, gpos<GM>(c0, m, sh, grid))));
+    if (rem > 1) {
+      const int c1 = rg.next();
+      acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[1]), gather_x<T>(x, gpos<GM>(c1, m, sh, grid))));
+    }
+    if (rem > 2) {
+      const int c2 = rg.next();
+      acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[2]), gather_x<T>(x, gpos<GM>(c2, m, sh, grid))));
+    }
+  }
+  return acc;
+}
+
+// d16 SpMV of a tomography A where the slices flagged in imp[] regenerate
+// their columns (RayGen) instead of reading the 16-bit deltas
+template <class V, class Tin, class T, bool POW2, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+sell_spmv_imp_kernel(long long rows, long long nslices, const long long* __restrict__ sptr,
+                     const int* __restrict__ rlen, const int* __restrict__ rbase, const short* __restrict__ dcol,
+                     const V* __restrict__ val, const Tin* __restrict__ xrow, const Tin* __restrict__ xT,
+                     const unsigned char* __restrict__ sflag, const unsigned char* __restrict__ imp, RayTab tb,
+                     int gshift, const int* __restrict__ sorder, unsigned int* __restrict__ sched,
+                     T* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int grid = tb.grid;
+  for (;;) {
+    unsigned int i = 0;
+    if (lane == 0) i = atomicAdd(&sched[0], 1u);
+    i = __shfl_sync(0xffffffffu, i, 0);
+    if (i >= nslices) break;
+    const long long s = sorder ? (long long)sorder[i] : (long long)i;
+    const bool tr = sflag != nullptr && sflag[s];
+    const bool im = imp[s] != 0;  // warp-uniform
+    const long long slot = s * 32 + lane;
+    const int len = rlen[slot];
+    const long long base = sptr[s];
+    const V* vp = val + base + lane * 4;
+    T acc;
+    if (im) {
+      RayGen rg;
+      rg.init(tb, slot < rows ? slot : 0);
+      if (!tr) acc = imp_row<0, V, Tin, T>(vp, rg, len, xrow, 0, 0, grid);
+      else if (POW2) acc = imp_row<1, V, Tin, T>(vp, rg, len, xT, grid - 1, gshift, grid);
+      else acc = imp_row<2, V, Tin, T>(vp, rg, len, xT, 0, 0, grid);
+    } else {
+      const short* dp = dcol + base + lane * 4;
+      const int c = rbase[slot];
+      if (!tr) acc = d16_row_u2<0, V, Tin, T>(dp, vp, c, len, xrow, 0, 0, grid);
+      else if (POW2) acc = d16_row_u2<1, V, Tin, T>(dp, vp, c, len, xT, grid - 1, gshift, grid);
+      else acc = d16_row_u2<2, V, Tin, T>(dp, vp, c, len, xT, 0, 0, grid);
+    }
+    if (slot < rows) y[slot] = acc;
+  }
+  if (lane == 0) {
+    __threadfence();
+    const unsigned int done = atomicAdd(&sched[1], 1u);
+    if (done == gridDim.x * (blockDim.x >> 5) - 1) {
+      sched[0] = 0;
+      sched[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
 template <class V, class Tin, class T, bool POW2, int DEPTH = 0>
 __global__ void __launch_bounds__(256, (DEPTH == 0 || DEPTH == 3) ? ((sizeof(T) == 4 && sizeof(V) == 4) ? 6 : 3)
                                        : DEPTH == 1 ? ((sizeof(T) == 4 && sizeof(V) == 4) ? 4 : 2)
