@@ -33,6 +33,7 @@
 #include "hs_krylov.cuh"
 #include "hs_loop.cuh"
 #include "hs_ops.cuh"
+#include "hs_c2.cuh"
 #include "hs_qr.cuh"
 #include "hs_shard.cuh"
 #include "hs_sketch.cuh"
@@ -222,6 +223,11 @@ bool env_flag(const char* name) {
   return e && *e && !(e[0] == '0' && e[1] == 0);
 }
 
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e && *e ? atoi(e) : dflt;
+}
+
 int grid_for(long long work, int block, int cap) {
   long long g = (work + block - 1) / block;
   if (g < 1) g = 1;
@@ -401,6 +407,10 @@ struct Sell {
   C8Geom c8g{0, 0};
   DBuf code, xoff, exc;
   long long n_exc = 0;
+  // 2-bit step codes on the slices flagged in c2ok (hs_c2.cuh); the rest keep their 16-bit deltas
+  bool c2 = false;
+  DBuf c2ok, c2tab, c2start, c2esc, c2code;
+  long long c2_slices = 0, c2_slots = 0;
   double index_bytes() const { return c8 ? 1.0 : d16 ? 2.0 : 4.0; }
   double slot_bytes() const { return c8 ? 12.0 : d16v ? 12.0 : d16 ? 8.0 : 4.0; }
   long long stored_values() const { return d16v ? n_explicit : nnz; }  // rlen (+ rbase) (+ escape offset) per slot
@@ -428,6 +438,44 @@ static bool sell_try_delta16(hs_ctx* ctx, Sell& S) {
   S.col.release();
   S.d16 = true;
   return true;
+}
+
+// 2-bit step codes for a tomography A (hs_c2.cuh), on the int32 image-order
+// columns before they become deltas.  A slice takes the codes when every row
+// of it needs at most two escapes; the others keep their 16-bit deltas, so
+// this only pays when sell_try_delta16 succeeds afterwards.  HS_C2=0 disables.
+static void sell_try_c2(hs_ctx* ctx, Sell& S, const unsigned char* sflag, int grid) {
+  if (S.nslices == 0 || S.col.p == nullptr || S.rperm.p != nullptr) return;
+  if (env_int("HS_C2", 1) == 0) return;
+  cudaStream_t s = ctx->stream;
+  const long long ns = S.nslots();
+  DBuf ok(S.nslices, true), tab(S.nslices * sizeof(int4), false), start(ns * sizeof(int), false),
+      esc(ns * sizeof(int4), false), code(S.slots / 4 + 96 * S.nslices + 128, true);
+  sell_c2_encode_kernel<<<grid_for(S.nslices, 8, 1 << 30), 256, 0, s>>>(
+      ns, S.nslices, S.sptr.as<long long>(), S.rlen.as<int>(), S.col.as<int>(), sflag, grid, ok.as<unsigned char>(),
+      tab.as<int4>(), start.as<int>(), esc.as<int4>(), code.as<unsigned char>());
+  CKL();
+  std::vector<unsigned char> hok(S.nslices);
+  std::vector<long long> hp(S.nslices + 1);
+  CK(cudaMemcpyAsync(hok.data(), ok.p, S.nslices, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hp.data(), S.sptr.p, (S.nslices + 1) * sizeof(long long), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  long long n_ok = 0, slots_ok = 0;
+  for (long long i = 0; i < S.nslices; ++i)
+    if (hok[i]) {
+      ++n_ok;
+      slots_ok += hp[i + 1] - hp[i];
+    }
+  // below half of the stream the mixed kernel is not worth its extra state
+  if (2 * slots_ok < S.slots) return;
+  S.c2ok = std::move(ok);
+  S.c2tab = std::move(tab);
+  S.c2start = std::move(start);
+  S.c2esc = std::move(esc);
+  S.c2code = std::move(code);
+  S.c2_slices = n_ok;
+  S.c2_slots = slots_ok;
+  S.c2 = true;
 }
 
 // Switch a d16 SELL copy to dominant-value flags (hs_ops.cuh: d16v) when at
@@ -654,9 +702,16 @@ struct hs_op {
       // algorithmic bytes of the stored encoding: values + column indices (4 B, or 2 B deltas)
       // + row lengths (+ row bases) + slice pointers + x once + y
       const bool impl = !transpose && imp_slices > 0 && M.d16 && !M.d16v && !M.c8;
+      // few slices of short rows: the d16 kernel's latency-bound schedules win (config 3); HS_C2=2 forces the codes
+      const bool few = M.nslices < 2LL * ctx->num_sms * 48 && (M.nslices > 0 ? M.slots / (M.nslices * 128) : 0) < 256;
+      const int c2env = M.c2 ? env_int("HS_C2", 1) : 0;
+      const bool c2 = !transpose && M.c2 && M.d16 && !M.d16v && !M.c8 && !impl && c2env != 0 && (!few || c2env == 2);
+      // c2 slices: a quarter byte of step codes per nonzero instead of the 2-byte delta, 16 B of escapes per row
+      const double c2frac = c2 ? (double)M.c2_slots / std::max<long long>(M.slots, 1) : 0.0;
       const double bytes = (double)M.stored_values() * sizeof(V) +
                            ((double)M.nnz - (impl ? (double)imp_slots * M.nnz / std::max<long long>(M.slots, 1) : 0.0)) *
-                               M.index_bytes() +
+                               M.index_bytes() * (1.0 - c2frac) +
+                           c2frac * ((double)M.nnz * 0.25 + (double)M.rows * 16.0) + (c2 ? (double)M.c2_slices * 16.0 : 0.0) +
                            (double)M.rows * M.slot_bytes() +
                            (double)M.n_exc * 4 + (double)M.nslices * 8 + (double)M.cols * sizeof(Tin) +
                            (double)M.rows * sizeof(T);
@@ -710,6 +765,20 @@ struct hs_op {
         } else {
           fail(HS_ERR_RUNTIME, "d16v SELL with non-fp32 values");
         }
+      } else if (c2) {
+        // 2-bit step codes on the conforming ray slices (hs_c2.cuh), 16-bit deltas elsewhere
+        int gshift = -1;
+        if (img_grid > 0 && (img_grid & (img_grid - 1)) == 0) gshift = __builtin_ctz((unsigned)img_grid);
+        const bool p2 = gshift >= 0 || !tflag;
+        constexpr bool F32 = sizeof(T) == 4 && sizeof(V) == 4;
+        constexpr int MINB = F32 ? 6 : 3;
+        auto kern = p2 ? sell_spmv_c2_kernel<V, Tin, T, true, MINB> : sell_spmv_c2_kernel<V, Tin, T, false, MINB>;
+        kern<<<grid, 256, 0, s>>>(M.rows, M.nslices, M.sptr.as<long long>(), M.rlen.as<int>(), M.rbase.as<int>(),
+                                  M.dcol.as<short>(), M.val.as<V>(), xi, tflag ? xT.as<Tin>() : nullptr,
+                                  tflag ? sflag.as<unsigned char>() : nullptr, M.c2ok.as<unsigned char>(),
+                                  M.c2tab.as<int4>(), M.c2start.as<int>(), M.c2esc.as<int4>(),
+                                  M.c2code.as<unsigned short>(), img_grid, gshift >= 0 ? gshift : 0,
+                                  M.sorder.as<int>(), M.sched.as<unsigned int>(), yo);
       } else if (impl) {
         // implicit columns on the verified ray slices (RayGen), 16-bit deltas elsewhere
         int gshift = -1;
