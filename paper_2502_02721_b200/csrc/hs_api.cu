@@ -411,6 +411,8 @@ struct Sell {
   bool c2 = false;
   DBuf c2ok, c2tab, c2start, c2esc, c2code;
   long long c2_slices = 0, c2_slots = 0;
+  bool t8 = false;    // A^T: 8-bit step codes (hs_c2.cuh: t8) on the flagged slices; shares the c2 buffers
+  int t8_bins = 0;
   double index_bytes() const { return c8 ? 1.0 : d16 ? 2.0 : 4.0; }
   double slot_bytes() const { return c8 ? 12.0 : d16v ? 12.0 : d16 ? 8.0 : 4.0; }
   long long stored_values() const { return d16v ? n_explicit : nnz; }  // rlen (+ rbase) (+ escape offset) per slot
@@ -476,6 +478,53 @@ static void sell_try_c2(hs_ctx* ctx, Sell& S, const unsigned char* sflag, int gr
   S.c2_slices = n_ok;
   S.c2_slots = slots_ok;
   S.c2 = true;
+}
+
+// 8-bit step codes for a tomography A^T (hs_c2.cuh: t8), from the int32
+// ray-order columns (before the sinogram layout mapping and the deltas).  The
+// caller then maps the columns to SinoBlk{n_bins, 4, 1, n_bins} and builds the
+// 16-bit deltas the non-conforming slices keep.  Opt-in (HS_T8=1; HS_T8=2 also
+// forces it on operators that take the latency-bound d16 schedules): config
+// 4's A^T moves 17% fewer bytes, bit-identical, and runs 3.55 against 3.62 ms
+// in isolation but 4.04 against 3.80 ms inside the solve -- A^T is bound by its
+// gather round trips (one per chunk per warp), and the table decode adds 14
+// instructions per chunk to a kernel that shares the SMs with the aux stream.
+static bool sell_try_t8(hs_ctx* ctx, Sell& S, int n_bins) {
+  if (S.nslices == 0 || S.col.p == nullptr || n_bins <= 0) return false;
+  const int mode = env_int("HS_T8", 0);
+  if (mode == 0) return false;
+  const bool few = S.nslices < 2LL * ctx->num_sms * 48 && S.slots / (S.nslices * 128) < 256;
+  if (few && mode != 2) return false;
+  if ((4LL * n_bins + 4 * 63) >= 32767) return false;  // the fallback slices' 16-bit deltas must hold a group step
+  cudaStream_t s = ctx->stream;
+  const long long ns = S.nslots();
+  DBuf ok(S.nslices, true), start(ns * sizeof(int), false), esc(ns * sizeof(int4), false),
+      code(std::max<long long>(S.slots, 4) + 128, true);
+  sell_t8_encode_kernel<<<grid_for(S.nslices, 8, 1 << 30), 256, 0, s>>>(
+      ns, S.nslices, S.sptr.as<long long>(), S.rlen.as<int>(), S.col.as<int>(), n_bins, ok.as<unsigned char>(),
+      start.as<int>(), esc.as<int4>(), code.as<unsigned char>());
+  CKL();
+  std::vector<unsigned char> hok(S.nslices);
+  std::vector<long long> hp(S.nslices + 1);
+  CK(cudaMemcpyAsync(hok.data(), ok.p, S.nslices, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hp.data(), S.sptr.p, (S.nslices + 1) * sizeof(long long), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  long long n_ok = 0, slots_ok = 0;
+  for (long long i = 0; i < S.nslices; ++i)
+    if (hok[i]) {
+      ++n_ok;
+      slots_ok += hp[i + 1] - hp[i];
+    }
+  if (2 * slots_ok < S.slots) return false;
+  S.c2ok = std::move(ok);
+  S.c2start = std::move(start);
+  S.c2esc = std::move(esc);
+  S.c2code = std::move(code);
+  S.c2_slices = n_ok;
+  S.c2_slots = slots_ok;
+  S.t8 = true;
+  S.t8_bins = n_bins;
+  return true;
 }
 
 // Switch a d16 SELL copy to dominant-value flags (hs_ops.cuh: d16v) when at
@@ -707,11 +756,13 @@ struct hs_op {
       const int c2env = M.c2 ? env_int("HS_C2", 1) : 0;
       const bool c2 = !transpose && M.c2 && M.d16 && !M.d16v && !M.c8 && !impl && c2env != 0 && (!few || c2env == 2);
       // c2 slices: a quarter byte of step codes per nonzero instead of the 2-byte delta, 16 B of escapes per row
-      const double c2frac = c2 ? (double)M.c2_slots / std::max<long long>(M.slots, 1) : 0.0;
+      const bool t8 = transpose && M.t8 && M.d16 && !M.c8;
+      const double c2frac = c2 || t8 ? (double)M.c2_slots / std::max<long long>(M.slots, 1) : 0.0;
       const double bytes = (double)M.stored_values() * sizeof(V) +
                            ((double)M.nnz - (impl ? (double)imp_slots * M.nnz / std::max<long long>(M.slots, 1) : 0.0)) *
                                M.index_bytes() * (1.0 - c2frac) +
-                           c2frac * ((double)M.nnz * 0.25 + (double)M.rows * 16.0) + (c2 ? (double)M.c2_slices * 16.0 : 0.0) +
+                           c2frac * ((double)M.nnz * (t8 ? 1.0 : 0.25) + (double)M.rows * 16.0) +
+                           (c2 ? (double)M.c2_slices * 16.0 : 0.0) +
                            (double)M.rows * M.slot_bytes() +
                            (double)M.n_exc * 4 + (double)M.nslices * 8 + (double)M.cols * sizeof(Tin) +
                            (double)M.rows * sizeof(T);
@@ -765,6 +816,14 @@ struct hs_op {
         } else {
           fail(HS_ERR_RUNTIME, "d16v SELL with non-fp32 values");
         }
+      } else if (t8) {
+        // 8-bit step codes over the 4-angle interleaved sinogram (hs_c2.cuh), 16-bit deltas elsewhere
+        constexpr bool F32 = sizeof(T) == 4 && sizeof(V) == 4;
+        constexpr int MINB = F32 ? 6 : 3;
+        sell_spmv_t8_kernel<V, Tin, T, MINB><<<grid, 256, 0, s>>>(
+            M.rows, M.nslices, M.sptr.as<long long>(), M.rlen.as<int>(), M.rbase.as<int>(), M.dcol.as<short>(),
+            M.val.as<V>(), xi, M.c2ok.as<unsigned char>(), M.c2start.as<int>(), M.c2esc.as<int4>(),
+            M.c2code.as<unsigned char>(), M.t8_bins, M.rperm.as<int>(), nullptr, M.sched.as<unsigned int>(), yo);
       } else if (c2) {
         // 2-bit step codes on the conforming ray slices (hs_c2.cuh), 16-bit deltas elsewhere
         int gshift = -1;
@@ -772,6 +831,7 @@ struct hs_op {
         const bool p2 = gshift >= 0 || !tflag;
         constexpr bool F32 = sizeof(T) == 4 && sizeof(V) == 4;
         constexpr int MINB = F32 ? 6 : 3;
+        // (8 blocks per SM, 32 registers with 40 B of spills: 3.17 against 2.78 ms)
         auto kern = p2 ? sell_spmv_c2_kernel<V, Tin, T, true, MINB> : sell_spmv_c2_kernel<V, Tin, T, false, MINB>;
         kern<<<grid, 256, 0, s>>>(M.rows, M.nslices, M.sptr.as<long long>(), M.rlen.as<int>(), M.rbase.as<int>(),
                                   M.dcol.as<short>(), M.val.as<V>(), xi, tflag ? xT.as<Tin>() : nullptr,

@@ -298,4 +298,206 @@ sell_spmv_c2_kernel(long long rows, long long nslices, const long long* __restri
   }
 }
 
+
+// ---- 8-bit step codes for a tomography A^T ("t8"): 5 instead of 6 B per nonzero --
+// A row of A^T is a pixel, and its sorted columns are the rays that cross it:
+// angle by angle, one to three neighbouring detector bins per angle.  With the
+// sinogram in the 4-angle interleave, address(a, b) = ((a >> 2) n_bins + b) 4
+// + (a & 3) (SinoBlk{n_bins, 4, 1, n_bins}: a 128-byte line holds 8 bins x 4
+// angles, the footprint of the 4 x 8 blocked layout), every step between
+// consecutive entries is one of
+//   code 0          : same angle, next bin              -> +4
+//   code 1 + D + 63 : next angle, bin shift D, same group of 4 angles -> 1 + 4 D
+//   code 128 + D+63 : next angle, bin shift D, next group             -> 4 n_bins - 3 + 4 D
+// (|D| <= 63), so one byte per entry indexes ONE 256-entry table shared by the
+// whole CTA (built at kernel start; the codes cluster on a few dozen
+// neighbouring entries, so the LDS is nearly conflict-free).  Anything else
+// (a pixel a detector misses at some angles) is an escape as in c2: code 0
+// plus a per-row (position, correction) pair, at most two per row, else the
+// slice keeps its 16-bit deltas in the same layout.
+__host__ __device__ __forceinline__ int t8_addr(int a, int b, int n_bins) { return ((a >> 2) * n_bins + b) * 4 + (a & 3); }
+
+__global__ void sell_t8_encode_kernel(long long nslots, long long nslices, const long long* __restrict__ sptr,
+                                      const int* __restrict__ rlen, const int* __restrict__ col, int n_bins,
+                                      unsigned char* __restrict__ ok, int* __restrict__ start, int4* __restrict__ esc,
+                                      unsigned char* __restrict__ code) {
+  const long long s = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (s >= nslices) return;
+  const int lane = threadIdx.x & 31;
+  const long long row = s * 32 + lane;
+  const int len = row < nslots ? rlen[row] : 0;
+  const long long base = sptr[s];
+  const int nq_slice = (int)((sptr[s + 1] - base) >> 7);
+  const int* cl = col + base + lane * 4;
+  auto col_at = [&](int e) { return cl[(long long)(e >> 2) * 128 + (e & 3)]; };
+  auto regular = [&](int da, int db) { return (da == 0 && db == 1) || (da == 1 && db >= -63 && db <= 63); };
+  int nesc = 0;
+  {
+    int pa = 0, pb = 0;
+    for (int e = 0; e < len; ++e) {
+      const int c = col_at(e), a = c / n_bins, b = c - a * n_bins;
+      if (e > 0 && !regular(a - pa, b - pb)) ++nesc;
+      pa = a;
+      pb = b;
+    }
+  }
+  const bool bad = __any_sync(0xffffffffu, nesc > 2);
+  if (lane == 0) ok[s] = bad ? 0 : 1;
+  if (bad) return;
+  int4 ev = make_int4(kC2NoEsc, 0, kC2NoEsc, 0);
+  unsigned char* cb = code + base + lane * 4;
+  int pa = 0, pb = 0, pg = 0, ne = 0;
+  for (int q = 0; q < nq_slice; ++q) {
+    unsigned w = 0;
+    for (int i = 0; i < 4; ++i) {
+      const int e = q * 4 + i;
+      if (e >= len) break;
+      const int c = col_at(e), a = c / n_bins, b = c - a * n_bins, g = t8_addr(a, b, n_bins);
+      if (e == 0) {
+        if (row < nslots) start[row] = g - 4;  // entry 0 carries code 0
+      } else {
+        const int da = a - pa, db = b - pb;
+        unsigned k = 0;
+        if (da == 0 && db == 1) {
+          k = 0;
+        } else if (da == 1 && db >= -63 && db <= 63) {
+          k = ((a & 3) == 0 ? 128u : 1u) + (unsigned)(db + 63);
+        } else {
+          const int fix = (g - pg) - 4;
+          if (ne == 0) { ev.x = e; ev.y = fix; }
+          else { ev.z = e; ev.w = fix; }
+          ++ne;
+        }
+        w |= k << (8 * i);
+      }
+      pa = a;
+      pb = b;
+      pg = g;
+    }
+    *reinterpret_cast<unsigned*>(cb + (long long)q * 128) = w;
+  }
+  if (len == 0 && row < nslots) start[row] = 0;
+  if (row < nslots) esc[row] = ev;
+}
+
+__device__ __forceinline__ int t8_step(unsigned k, int n_bins) {
+  if (k == 0) return 4;
+  if (k < 128) return 1 + 4 * ((int)k - 1 - 63);
+  if (k < 255) return 4 * n_bins - 3 + 4 * ((int)k - 128 - 63);
+  return 0;
+}
+
+__device__ __forceinline__ int t8_lds(unsigned addr) {
+  int r;
+  asm("ld.shared.s32 %0, [%1];" : "=r"(r) : "r"(addr) : "memory");
+  return r;
+}
+
+// the chunk's four steps: byte j of w indexes the 1024-byte-aligned table at shared address tab
+__device__ __forceinline__ void t8_addrs(int a, unsigned w, unsigned tab, int (&ad)[4]) {
+  const int s0 = t8_lds(tab | ((w << 2) & 0x3fcu)), s1 = t8_lds(tab | ((w >> 6) & 0x3fcu)),
+            s2 = t8_lds(tab | ((w >> 14) & 0x3fcu)), s3 = t8_lds(tab | ((w >> 22) & 0x3fcu));
+  ad[0] = a + s0;
+  ad[1] = ad[0] + s1;
+  ad[2] = ad[1] + s2;
+  ad[3] = ad[2] + s3;
+}
+
+template <class V, class Tin, class T>
+__device__ __forceinline__ void t8_chunk(T& acc, int& a, unsigned w, unsigned tab, const Chunk4<V>& v,
+                                         const Tin* __restrict__ x, int q, int& eq, const int4* __restrict__ escp) {
+  int ad[4];
+  t8_addrs(a, w, tab, ad);
+  if (q == eq) c2_escape(q, eq, escp, ad);
+  const T x0 = gather_x<T>(x, ad[0]);
+  const T x1 = gather_x<T>(x, ad[1]);
+  const T x2 = gather_x<T>(x, ad[2]);
+  const T x3 = gather_x<T>(x, ad[3]);
+  acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[0]), x0));
+  acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[1]), x1));
+  acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[2]), x2));
+  acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[3]), x3));
+  a = ad[3];
+}
+
+// one lane's row: the next chunk's (codes, values) in flight while a chunk is
+// decoded, gathered and added (the d16_row_u2 schedule)
+template <class V, class Tin, class T>
+__device__ __forceinline__ T t8_row(const unsigned* __restrict__ cp, const V* __restrict__ vp, int a, int len,
+                                    const Tin* __restrict__ x, unsigned tab, const int4* __restrict__ escp, int eq) {
+  T acc = T(0);
+  const int nq = (len + 3) >> 2, nfull = len >> 2;
+  if (nq == 0) return acc;
+  unsigned w = __ldcs(cp);
+  Chunk4<V> v = Chunk4<V>::load(vp);
+#pragma unroll 2
+  for (int q = 0; q < nfull; ++q) {
+    const long long qn = min(q + 1, nq - 1);
+    const unsigned wn = __ldcs(cp + qn * 32);
+    const Chunk4<V> vn = Chunk4<V>::load(vp + qn * 128);
+    t8_chunk<V, Tin, T>(acc, a, w, tab, v, x, q, eq, escp);
+    w = wn;
+    v = vn;
+  }
+  const int rem = len & 3;
+  if (rem) {
+    int ad[4];
+    t8_addrs(a, w, tab, ad);
+    if (nfull == eq) c2_escape(nfull, eq, escp, ad);
+    acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[0]), gather_x<T>(x, ad[0])));
+    if (rem > 1) acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[1]), gather_x<T>(x, ad[1])));
+    if (rem > 2) acc = Rn<T>::add(acc, Rn<T>::mul(cvt<T>(v.v[2]), gather_x<T>(x, ad[2])));
+  }
+  return acc;
+}
+
+// SpMV of a tomography A^T over the 4-angle interleaved sinogram: slices
+// flagged in ok decode 8-bit step codes, the rest their 16-bit deltas (same
+// layout).  rperm: slot -> pixel (8 x 4 tiles).  Natural slice order.
+template <class V, class Tin, class T, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+sell_spmv_t8_kernel(long long rows, long long nslices, const long long* __restrict__ sptr,
+                    const int* __restrict__ rlen, const int* __restrict__ rbase, const short* __restrict__ dcol,
+                    const V* __restrict__ val, const Tin* __restrict__ x, const unsigned char* __restrict__ ok,
+                    const int* __restrict__ start, const int4* __restrict__ esc,
+                    const unsigned char* __restrict__ code, int n_bins, const int* __restrict__ rperm,
+                    const int* __restrict__ sorder, unsigned int* __restrict__ sched, T* __restrict__ y) {
+  __shared__ __align__(1024) int tab_s[256];
+  tab_s[threadIdx.x] = t8_step(threadIdx.x, n_bins);
+  __syncthreads();
+  const unsigned tab = smem_u32(tab_s);
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    unsigned int i = 0;
+    if (lane == 0) i = atomicAdd(&sched[0], 1u);
+    i = __shfl_sync(0xffffffffu, i, 0);
+    if (i >= nslices) break;
+    const long long s = sorder ? (long long)sorder[i] : (long long)i;
+    const long long slot = s * 32 + lane;
+    const long long row = rperm ? (long long)rperm[slot] : slot;
+    const int len = rlen[slot];
+    const long long base = sptr[s];
+    const V* vp = val + base + lane * 4;
+    T acc;
+    if (ok[s]) {  // warp-uniform
+      const int4* escp = esc + slot;
+      const int e0 = __ldg(&escp->x);
+      acc = t8_row<V, Tin, T>(reinterpret_cast<const unsigned*>(code + base) + lane, vp, start[slot], len, x, tab, escp,
+                              e0 == kC2NoEsc ? kC2NoEsc : (e0 >> 2));
+    } else {
+      acc = d16_row_u2<0, V, Tin, T>(dcol + base + lane * 4, vp, rbase[slot], len, x, 0, 0, 0);
+    }
+    if (row >= 0 && row < rows) y[row] = acc;
+  }
+  if (lane == 0) {
+    __threadfence();
+    const unsigned int done = atomicAdd(&sched[1], 1u);
+    if (done == gridDim.x * (blockDim.x >> 5) - 1) {
+      sched[0] = 0;
+      sched[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
 }  // namespace hs

@@ -139,9 +139,10 @@ def test_tomography_builder_general_bins(hs, grid, angles, bins):
     "env",
     [{}, {"HS_C8": "1"}, {"HS_AT_C8": "1"}, {"HS_SINO_BLK": "0"}, {"HS_C8": "1", "HS_SINO_BLK": "2x16"},
      {"HS_D16_PIPE": "0"}, {"HS_D16_PIPE": "1"}, {"HS_D16_PIPE": "2"}, {"HS_D16_PIPE": "4"},
-     {"HS_D16_PIPE": "8"}, {"HS_D16_PIPE": "3"}, {"HS_D16V": "1", "HS_D16V_FORCE": "1"}, {"HS_C2": "2"}],
+     {"HS_D16_PIPE": "8"}, {"HS_D16_PIPE": "3"}, {"HS_D16V": "1", "HS_D16V_FORCE": "1"}, {"HS_C2": "2"},
+     {"HS_T8": "2"}, {"HS_C2": "2", "HS_T8": "2"}],
     ids=["default", "a_c8", "at_c8", "ray_order", "a_c8_blk2x16", "d16_depth0", "d16_depth1", "d16_depth2",
-         "d16_depth4", "d16_ring", "d16_unrolled", "d16v", "a_c2"],
+         "d16_depth4", "d16_ring", "d16_unrolled", "d16v", "a_c2", "at_t8", "a_c2_at_t8"],
 )
 def test_tomography_encodings_bitwise(hs, monkeypatch, grid, angles, bins, env):
     """Every device encoding of the tomography operator (8-bit transition codes
@@ -153,8 +154,8 @@ def test_tomography_encodings_bitwise(hs, monkeypatch, grid, angles, bins, env):
     each lane-pipeline depth of the 16-bit-delta kernel (0: config 4's, 1-2:
     the few-slice schedules, 4: the deepest, 8: the cp.async ring);
     HS_D16V + HS_D16V_FORCE put A on the opt-in dominant-value-flag encoding;
-    HS_C2=2 forces A's 2-bit step codes (the default at config-4 size) on these
-    small operators."""
+    HS_C2=2 / HS_T8=2 force A's 2-bit and A^T's 8-bit step codes (the defaults
+    at config-4 size) on these small operators."""
     import scipy.sparse as sp
 
     from oracle import cpu_baseline as cb
