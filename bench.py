@@ -304,6 +304,7 @@ def run_ours(args, ws, rank, local):
         "roofline": (dict(rl[dom], peak_source=peak_kind,
                           other_spmv=rl["spmv_A" if dom == "spmv_AT" else "spmv_AT"])
                      if dom else None),
+        "storage": ({"A": op.storage(False), "AT": op.storage(True)} if hasattr(op, "storage") else None),
         "gpu_launches": int(launches),
         "clocks": clocks,
         "kernels": kernels,

@@ -145,6 +145,13 @@ int hs_op_psf_create(hs_ctx* ctx, int64_t height, int64_t width, int32_t kh, int
 int hs_op_tomo_create(hs_ctx* ctx, int32_t grid, int32_t n_angles, int32_t n_bins, const double* cos_t,
                       const double* sin_t, const double* offsets, int vdtype, hs_op** out);
 int hs_op_info(const hs_op* op, int64_t* m, int64_t* n, int64_t* nnz, int64_t* nnz_t);
+/* storage of the SELL copy one direction runs on (no reference counterpart: the
+   reference keeps scipy CSR, linops.py:137-141): slices, entry slots (with
+   padding), slices / slots on compact step codes (2-bit for A, 8-bit for A^T),
+   and the stored index bytes per nonzero (4 int32, 2 deltas, 1 or 0.25 codes,
+   averaged over the slices).  Zeros for operators without a SELL copy. */
+int hs_op_storage(const hs_op* op, int transpose, int64_t* slices, int64_t* slots, int64_t* code_slices,
+                  int64_t* code_slots, double* index_bytes_per_nnz);
 /* y = A x (transpose = 0) or A^T x (transpose = 1); x, y host float64 or float32 (= work dtype) */
 int hs_op_apply(hs_op* op, int transpose, int work_dtype, const void* x, void* y);
 /* copy the device CSR (transpose selects A^T) to host buffers (data as float64) */

@@ -73,6 +73,7 @@ _SIGNATURES = [
     ("hs_op_psf_create", c_i32, [c_vp, c_i64, c_i64, c_i32, c_i32, c_vp, ctypes.c_int, ctypes.POINTER(c_vp)]),
     ("hs_op_tomo_create", c_i32, [c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.POINTER(c_vp)]),
     ("hs_op_info", c_i32, [c_vp, P_i64, P_i64, P_i64, P_i64]),
+    ("hs_op_storage", c_i32, [c_vp, c_i32, P_i64, P_i64, P_i64, P_i64, ctypes.POINTER(ctypes.c_double)]),
     ("hs_op_apply", c_i32, [c_vp, ctypes.c_int, ctypes.c_int, c_vp, c_vp]),
     ("hs_op_export_csr", c_i32, [c_vp, ctypes.c_int, c_vp, c_vp, c_vp]),
     ("hs_op_destroy", c_i32, [c_vp]),

@@ -174,6 +174,16 @@ class DeviceOperator(LinearOperator):
         _lib.check(_lib.load().hs_op_info(self._handle, ctypes.byref(m), ctypes.byref(n), ctypes.byref(nnz), ctypes.byref(nnzt)))
         return {"rows": m.value, "cols": n.value, "nnz": nnz.value, "nnz_t": nnzt.value}
 
+    def storage(self, transpose=False):
+        """How the SELL copy of A (or A^T) is stored on the device: slices, entry
+        slots, the slices / slots on compact step codes, index bytes per nonzero."""
+        sl, so, cs, co = _lib.c_i64(), _lib.c_i64(), _lib.c_i64(), _lib.c_i64()
+        ib = ctypes.c_double()
+        _lib.check(_lib.load().hs_op_storage(self._handle, 1 if transpose else 0, ctypes.byref(sl), ctypes.byref(so),
+                                             ctypes.byref(cs), ctypes.byref(co), ctypes.byref(ib)))
+        return {"slices": sl.value, "slots": so.value, "code_slices": cs.value, "code_slots": co.value,
+                "index_bytes_per_nnz": ib.value}
+
     def __del__(self):
         if getattr(self, "_owner", None) is None and getattr(self, "_handle", None) is not None:
             try:

@@ -181,6 +181,44 @@ def test_tomography_encodings_bitwise(hs, monkeypatch, grid, angles, bins, env):
     np.testing.assert_array_equal(op.rmatvec(y.astype(np.float64), np.float64), St @ y.astype(np.float64))
 
 
+def test_tomography_step_code_storage(hs, monkeypatch):
+    """The step-code encoders (hs_c2.cuh) take the ray slices of A (2-bit codes,
+    default) and, when asked, the pixel tiles of A^T (8-bit codes): nearly every
+    slice of a full-coverage geometry conforms, the stored index bytes per
+    nonzero drop from 2 to ~0.25 / ~1, and a slice whose rows need more than
+    two escapes keeps its deltas (a detector narrower than the image diagonal
+    leaves corner pixels unseen over a range of angles)."""
+    op = hs.TomographyOperator(192, 360, 273, dtype=np.float32)
+    a, at = op.storage(False), op.storage(True)
+    assert a["slices"] == (360 * 273 + 31) // 32
+    assert a["code_slices"] >= 0.95 * a["slices"]
+    assert a["index_bytes_per_nnz"] < 0.5
+    assert at["code_slices"] == 0 and at["index_bytes_per_nnz"] == 2.0
+    monkeypatch.setenv("HS_T8", "2")
+    monkeypatch.setenv("HS_C2", "0")
+    op2 = hs.TomographyOperator(192, 360, 273, dtype=np.float32)
+    a2, at2 = op2.storage(False), op2.storage(True)
+    assert a2["code_slices"] == 0 and a2["index_bytes_per_nnz"] == 2.0
+    assert at2["code_slices"] >= 0.95 * at2["slices"]
+    assert at2["index_bytes_per_nnz"] < 1.1
+    # both directions still apply the same matrix
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal(op.cols).astype(np.float32)
+    y = rng.standard_normal(op.rows).astype(np.float32)
+    np.testing.assert_array_equal(op.matvec(x, np.float32), op2.matvec(x, np.float32))
+    np.testing.assert_array_equal(op.rmatvec(y, np.float32), op2.rmatvec(y, np.float32))
+    # narrow detector: pixels near the corners are missed at several angles
+    monkeypatch.setenv("HS_C2", "2")
+    op3 = hs.TomographyOperator(96, 180, 97, dtype=np.float32)
+    monkeypatch.setenv("HS_C2", "0")
+    monkeypatch.setenv("HS_T8", "0")
+    op4 = hs.TomographyOperator(96, 180, 97, dtype=np.float32)
+    x = rng.standard_normal(op3.cols).astype(np.float32)
+    y = rng.standard_normal(op3.rows).astype(np.float32)
+    np.testing.assert_array_equal(op3.matvec(x, np.float32), op4.matvec(x, np.float32))
+    np.testing.assert_array_equal(op3.rmatvec(y, np.float32), op4.rmatvec(y, np.float32))
+
+
 # ---------------------------------------------------------------------------
 # sketches
 
