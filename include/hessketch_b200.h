@@ -117,6 +117,10 @@ int hs_ctx_synchronize(hs_ctx* ctx);
 /* multi-GPU: NCCL communicator over `nranks` processes (one per GPU) */
 int hs_comm_get_unique_id(void* out_128_bytes);
 int hs_comm_init(hs_ctx* ctx, int nranks, int rank, const void* unique_id_128_bytes);
+/* runs every NCCL call the sharded loops make (all-gather, fp64 all-reduce,
+   grouped send/recv) on a throwaway one-rank communicator and checks the
+   results: verifies the run-time NCCL bindings on a single GPU */
+int hs_nccl_selftest(hs_ctx* ctx);
 int hs_comm_info(const hs_ctx* ctx, int32_t* nranks, int32_t* rank);
 /* in-process ranks: contexts ctxs[0..nranks) become ranks 0..nranks-1 of one
    communicator whose collectives are stream-ordered device copies between the

@@ -63,6 +63,7 @@ _SIGNATURES = [
     ("hs_ctx_kernel_names", c_i32, [c_vp, ctypes.c_char_p, c_i64]),
     ("hs_comm_get_unique_id", c_i32, [c_vp]),
     ("hs_comm_init", c_i32, [c_vp, ctypes.c_int, ctypes.c_int, c_vp]),
+    ("hs_nccl_selftest", c_i32, [c_vp]),
     ("hs_comm_info", c_i32, [c_vp, P_i32, P_i32]),
     ("hs_comm_init_local", c_i32, [ctypes.POINTER(c_vp), ctypes.c_int]),
     ("hs_comm_abort", c_i32, [c_vp]),

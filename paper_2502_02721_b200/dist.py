@@ -23,7 +23,7 @@ from dataclasses import dataclass
 
 from . import _lib
 
-__all__ = ["ShardPlan", "shard_plan", "psf_shard_plan", "shard_granule", "sketch_tile", "init_comm", "comm_info",
+__all__ = ["ShardPlan", "shard_plan", "psf_shard_plan", "shard_granule", "sketch_tile", "init_comm", "nccl_selftest", "comm_info",
            "local_group", "run_ranks"]
 
 
@@ -107,6 +107,13 @@ def init_comm(ctx=None):
     raw = ctypes.create_string_buffer(box[0], 128)
     _lib.check(lib.hs_comm_init(ctx.handle, ws, rank, raw))
     return ws, rank
+
+
+def nccl_selftest(ctx=None):
+    """Run every NCCL call of the sharded loops on a one-rank communicator on
+    this context's GPU and check the results (raises on any mismatch)."""
+    ctx = ctx or _lib.context()
+    _lib.check(_lib.load().hs_nccl_selftest(ctx.handle))
 
 
 def comm_info(ctx=None):

@@ -134,3 +134,14 @@ def test_local_ranks_failure_releases_peers(hs):
 
     with pytest.raises((ValueError, RuntimeError)):
         _ranks(2, rank)
+
+
+def test_nccl_bindings_single_rank(hs):
+    """The run-time NCCL bindings (dlopen'ed libnccl.so.2: all-gather, fp64 sum
+    all-reduce, grouped send/recv -- every call hs_dist.inc makes) on a one-rank
+    communicator: results checked inside the library.  Two ranks cannot share
+    one GPU under NCCL, so the P-rank data path itself is covered by the
+    in-process ranks above."""
+    from paper_2502_02721_b200 import dist as hsd
+
+    hsd.nccl_selftest()
