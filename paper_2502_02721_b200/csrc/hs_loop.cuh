@@ -497,14 +497,36 @@ xpass_kernel(long long n, const B* __restrict__ basis, long long ld, int kx, con
   for (int i = threadIdx.x; i < kx; i += blockDim.x) ys[i] = y[i];
   __syncthreads();
   double sq = 0.0;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
-    double xa = 0.0;
-    for (int j = 0; j < kx; ++j) xa = fma(ys[j], cvt<double>(basis[(long long)j * ld + e]), xa);
-    const double xe = xa + (x0 ? x0[e] : 0.0);
-    if (xout) xout[e] = xe;
-    if (xt) {
-      const double d = xe - xt[e];
-      sq = fma(d, d, sq);
+  // VEC consecutive elements per thread, one 16-byte load per basis column and
+  // eight columns in flight (the columns are padded to ld >= n rounded up to
+  // 64, so a strip may read past n); per element the sum is still j-ascending
+  constexpr int VEC = 16 / sizeof(B);
+  const long long nvec = (n + VEC - 1) / VEC;
+  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += (long long)gridDim.x * blockDim.x) {
+    const long long e0 = v * VEC;
+    double xa[VEC];
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) xa[q] = 0.0;
+    const B* bp = basis + e0;
+#pragma unroll 8
+    for (int j = 0; j < kx; ++j) {
+      B b[VEC];
+      VecLoad<B, VEC>::ld(bp + (long long)j * ld, b);
+      const double yj = ys[j];
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) xa[q] = fma(yj, cvt<double>(b[q]), xa[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) {
+      const long long e = e0 + q;
+      if (e < n) {
+        const double xe = xa[q] + (x0 ? x0[e] : 0.0);
+        if (xout) xout[e] = xe;
+        if (xt) {
+          const double d = xe - xt[e];
+          sq = fma(d, d, sq);
+        }
+      }
     }
   }
   if (!xt) return;
