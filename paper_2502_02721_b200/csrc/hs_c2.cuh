@@ -205,7 +205,9 @@ __device__ __forceinline__ void c2_chunk(T& acc, int& a, unsigned w, unsigned ta
 // whole next pair up front 2.99 ms (3.02 at 5 blocks per SM without spills):
 // without the per-chunk branch ptxas sinks the stream loads below the first
 // gather stall, and the loads in flight per warp, not the issue slots, bound
-// this kernel.)
+// this kernel.  Pinning the order with ld.volatile stream loads and table
+// reads: 2.96 ms; one warp-uniform escape vote per pair selecting a checked or
+// an unchecked copy of the pair: 3.03 ms.)
 template <class V, class Tin, class T>
 __device__ __forceinline__ T c2_row(const unsigned short* __restrict__ cp, const V* __restrict__ vp, int a, int len,
                                     const Tin* __restrict__ x, unsigned tab, const int4* __restrict__ escp, int eq) {

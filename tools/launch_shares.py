@@ -9,7 +9,8 @@ import sys
 from collections import defaultdict
 
 SETUP = ("tomo_", "csr_", "cub::", "sell_fill", "sino_block_cols", "sell_delta", "sell_transpose_cols",
-         "sell_slice", "tile_perm", "sparse_sign_gen", "i64_to_u64", "u32_to_i64", "sell_c8_encode")
+         "sell_slice", "tile_perm", "sparse_sign_gen", "i64_to_u64", "u32_to_i64", "sell_c8_encode", "sell_c2_encode",
+         "sell_t8_encode")
 loop_only = "--loop-only" in sys.argv
 rows = [r for r in csv.reader(open(sys.argv[1])) if r]
 hdr = None
