@@ -1,7 +1,8 @@
 """Out-of-bounds-write check of every kernel family (compute-sanitizer is not
 available on the GPU pool): with HS_GUARD=1 each device buffer carries 4 KB
 guard bands on both sides, verified when the buffer is released.  A battery of
-small solves covering the operators (CSR / SELL encodings, PSF stencils,
+small solves covering the operators (CSR / SELL encodings incl. the step
+codes, PSF stencils,
 dense), the fused elimination pass, fsub, pivot commit, normalisation, the
 sketches (sparse-sign tiles, Gaussian batches, dense), the cooperative
 projected solve, sampled pivoting, the step API, GMRES / LSQR, diagnostics and
@@ -39,6 +40,17 @@ def test_no_out_of_bounds_writes(monkeypatch):
         hs.slslu(op, b, cfg, x_true=x)
         hs.lslu(op, b, hs.SolverConfig(maxiter=K, dtype=dt), x_true=x)
         hs.lsqr(op, b, hs.SolverConfig(maxiter=K, dtype=dt), x_true=x)
+    # the step-code encoders and kernels (2-bit on A, 8-bit on A^T), forced on a small operator
+    monkeypatch.setenv("HS_C2", "2")
+    monkeypatch.setenv("HS_T8", "2")
+    for g2, a2, b2 in ((48, 30, 69), (50, 33, 41)):
+        opc = hs.TomographyOperator(g2, a2, b2, dtype=np.float32)
+        xc = random_ellipses(g2, 10, 0).ravel()
+        bc, _ = add_noise(opc.matvec(xc), 0.01, 1)
+        hs.slslu(opc, bc, hs.SolverConfig(maxiter=K, dtype="float32"), x_true=xc)
+        del opc
+    monkeypatch.delenv("HS_C2")
+    monkeypatch.delenv("HS_T8")
     size = 64
     psf = gaussian_psf(2.0, radius=7)
     xi = rectangles_and_discs(size, 20, 0).ravel()
