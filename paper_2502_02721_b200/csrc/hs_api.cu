@@ -1845,6 +1845,46 @@ struct Solver {
       CKL();
     };
 
+    // Short vectors (configs 1-3): the whole basis step -- forward substitution,
+    // elimination pass, commit, normalisation -- as ONE cooperative kernel
+    // (hs_loop.cuh: basis_step_kernel) instead of four latency-bound launches.
+    // Not with sampled pivoting (its pick runs between the pass and the commit).
+    // Measured (tools/run_configs.py, loop it/s without per-kernel events): config 1 (n = 1024) 17.2k ->
+    // 20.3k, config 2 (n = 65,536) 14.6k -> 15.1k; config 3 (n = 262,144: 2.92k -> 2.84k) keeps the
+    // separate kernels -- there the pass wants more blocks than a cooperative grid holds, and the step
+    // is bound by the dependent chains inside the phases, not by the launches.
+    const long long step_fuse_max = env_int("HS_STEP_FUSE_MAX", 65536);
+    auto step_fusable = [&](long long len) {
+      return ps <= 0 && !env_flag("HS_NO_STEP_FUSE") && len <= step_fuse_max && !env_flag("HS_ELIM_VEC");
+    };
+    auto step_fused = [&](const T* uin, T* P, double* hcol, long long len, long long ldv, const B* basis, T* uout,
+                          int k, int side, int iter, int kx, const double* yx, double* relerr_slot, long long dim,
+                          long long* pos, T* pivval, bool do_norm, B* dst, SinoBlk blk, B* yb) {
+      StepArgs<T, B> a;
+      a.u = uin; a.P = P; a.Pw = P; a.ldp = ldp; a.k = k; a.c = cvec.as<T>(); a.hcol = hcol;
+      a.n = len; a.ld = ldv; a.basis = basis; a.uo = uout; a.kx = kx; a.yx = yx;
+      a.x0 = x0_h ? x0d.as<double>() : nullptr; a.xt = kx ? xtd.as<double>() : nullptr;
+      a.xpart = xpart.as<double>(); a.relerr_out = relerr_slot; a.cand = candp.as<Cand>();
+      a.dim = dim; a.pos = pos; a.pivval = pivval;
+      a.do_norm = do_norm ? 1 : 0; a.n_pad = ldv; a.dst = dst; a.blk = blk; a.yb = yb;
+      a.st = st; a.side = side; a.iter = iter;
+      const size_t smem = basis_step_smem(k, kx, sizeof(T));
+      auto kern = kx ? basis_step_kernel<T, B, true> : basis_step_kernel<T, B, false>;
+      // (the kernel's ~1 KB of static shared memory counts against the 48 KB default too)
+      CK(ensure_smem((const void*)kern, smem > 40 * 1024 ? std::max<size_t>(smem, 64 * 1024) : smem));
+      // two blocks per SM at most: the projected solve's cooperative grid runs beside this one
+      int per_sm = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)kern, 256, smem));
+      if (per_sm < 1) fail(HS_ERR_RUNTIME, "basis step kernel does not fit an SM (%zu B of shared memory)", smem);
+      const int g = (int)std::min<long long>((len + 255) / 256, std::min(std::min(2, per_sm) * SMS, CAND_CAP));
+      const double bytes = (double)std::max(k, kx) * len * sizeof(B) + 4.0 * len * sizeof(T) +
+                           (kx ? (double)len * 8 : 0.0);
+      Prof p(ctx, side == 0 && !square ? "step_D" : "step_L", bytes);
+      void* args[] = {(void*)&a};
+      CK(cudaLaunchCooperativeKernel((void*)kern, dim3(g), dim3(256), args, smem, s));
+      ++g_launches;
+    };
+
     // Two streams (column sketching): the sketch of u = A l_k and the projected
     // solve of iteration k run on ctx->aux while the main stream does the
     // basis work; u is not overwritten by the elimination (it writes u2), the
@@ -1996,6 +2036,16 @@ struct Solver {
         if (ovl && kx) CK(cudaStreamWaitEvent(s, SB > 1 ? ev_qrb[(kx - 1) / SB] : ev_qr, 0));
       };
       if (!square) {
+        // d_{k+1}, and the same values in the blocked sinogram layout A^T gathers from
+        B* ybk = reinterpret_cast<B*>(op->blocked_input(sizeof(B)));
+        if (env_flag("HS_NO_YB_FUSE")) ybk = nullptr;
+        if (step_fusable(m)) {
+          step_fused(ucur, PD.as<T>(), Hcol(k - 1), m, ldm, D, uel, k, 0, k, 0, nullptr, nullptr, m,
+                     tpos.as<long long>(), pv.as<T>(), true, Dcol(k), op->sblk, ybk);
+          if (!skd)
+            CK(cudaMemcpyAsync(Zb.as<double>() + (long long)(k - 1) * ell, Hcol(k - 1),
+                               (size_t)(k + 1) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        } else {
         fsub(ucur, tpos.as<long long>(), PD.as<T>(), ldp, k, k, 0, cvec.as<T>(), Hcol(k - 1));
         elim(ucur, m, ldm, D, k, 0, k, 0, nullptr, nullptr, uel);
         sample(uel, m, k, 2 * k, 0, k);
@@ -2006,17 +2056,21 @@ struct Solver {
         if (!skd)
           CK(cudaMemcpyAsync(Zb.as<double>() + (long long)(k - 1) * ell, Hcol(k - 1), (size_t)(k + 1) * sizeof(double),
                              cudaMemcpyDeviceToDevice, s));
-        // d_{k+1}, and the same values in the blocked sinogram layout A^T gathers from
-        B* ybk = reinterpret_cast<B*>(op->blocked_input(sizeof(B)));
-        if (env_flag("HS_NO_YB_FUSE")) ybk = nullptr;
         normalize_kernel<T, B><<<grid_for(ldm, 256, NORM_G), 256, 0, s>>>(m, ldm, uel, pv.as<T>(), Dcol(k), st, 0, k,
                                                                           op->sblk, ybk);
         CKL();
+        }
         if (defer_sk) sketch_u();
         if (sb) S2->apply(Dcol(k), bdt, Gb.as<double>() + (long long)k * ell, skM, G2);
         op->apply(Dcol(k), bdt, q.p, wdt, true, ybk != nullptr);
         // printed variant: F column k = S1 q before the elimination (solvers.py:488-490)
         if (printed) S1->apply(q.p, wdt, Fb.as<double>() + (long long)k * ell, skM, G1);
+        const bool fuse_l = step_fusable(n);
+        if (fuse_l) {
+          wait_y();
+          step_fused(q.as<T>(), PL.as<T>(), Wcol(k), n, ldn, L, q.as<T>(), k, 1, k, kx, yprev, relslot, n,
+                     gpos.as<long long>(), pv.as<T>() + 1, lT == nullptr, Lcol(k), SinoBlk{0, 0, 0, 0}, nullptr);
+        } else {
         fsub(q.as<T>(), gpos.as<long long>(), PL.as<T>(), ldp, k, k, 1, cvec.as<T>(), Wcol(k));
         wait_y();
         elim(q.as<T>(), n, ldn, L, k, 1, k, kx, yprev, relslot, q.as<T>());
@@ -2025,7 +2079,10 @@ struct Solver {
                                                     n, st, 1, k, pv.as<T>() + 1);
         CKL();
         swap_perm(1, k);
-        if (lT) {
+        }
+        if (fuse_l && !lT) {
+          // normalised inside the step kernel
+        } else if (lT) {
           const dim3 tg((op->img_grid + 31) / 32, (op->img_grid + 31) / 32);
           normalize_transpose_kernel<T, B><<<tg, 256, 0, s>>>(op->img_grid, ldn, q.as<T>(), pv.as<T>() + 1, Lcol(k),
                                                               lT, st, k);
@@ -2037,6 +2094,14 @@ struct Solver {
         lT_ready = lT != nullptr;
       } else {
         if (skd && !ovl && !sb) S2->apply(u.p, wdt, Zb.as<double>() + (long long)(k - 1) * ell, skM, G2);
+        if (step_fusable(n)) {
+          wait_y();
+          step_fused(ucur, PL.as<T>(), Hcol(k - 1), n, ldn, L, uel, k, 0, k, kx, yprev, relslot, n,
+                     tpos.as<long long>(), pv.as<T>(), true, Lcol(k), SinoBlk{0, 0, 0, 0}, nullptr);
+          if (!skd)
+            CK(cudaMemcpyAsync(Zb.as<double>() + (long long)(k - 1) * ell, Hcol(k - 1),
+                               (size_t)(k + 1) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        } else {
         fsub(ucur, tpos.as<long long>(), PL.as<T>(), ldp, k, k, 0, cvec.as<T>(), Hcol(k - 1));
         wait_y();
         elim(ucur, n, ldn, L, k, 0, k, kx, yprev, relslot, uel);
@@ -2050,6 +2115,7 @@ struct Solver {
                              cudaMemcpyDeviceToDevice, s));
         normalize_kernel<T, B><<<grid_for(ldn, 256, NORM_G), 256, 0, s>>>(n, ldn, uel, pv.as<T>(), Lcol(k), st, 0, k);
         CKL();
+        }
         if (sb) S2->apply(Lcol(k), bdt, Gb.as<double>() + (long long)k * ell, skM, G2);
       }
       if (sb) {

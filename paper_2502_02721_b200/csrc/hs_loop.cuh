@@ -13,6 +13,10 @@
 //   xpass_kernel          x = x0 + L_k y with the relative error partials (solvers.py:236-240)
 #pragma once
 
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
 #include "hs_common.cuh"
 
 namespace hs {
@@ -147,6 +151,14 @@ __device__ __forceinline__ void fsub_panel_copy(const T* __restrict__ P, int ldp
 
 inline size_t fsub_panel_smem(int k, size_t tsize) { return ((size_t)k + 2 * 32 * (size_t)k) * tsize; }
 
+// the whole forward substitution, run by every thread of ONE block (smem_raw:
+// fsub_panel_smem(k) bytes, 128-byte aligned)
+template <class T>
+__device__ __forceinline__ void fsub_panel_body(const T* __restrict__ u, const long long* __restrict__ pos,
+                                                long long pos_offset, const T* __restrict__ P, int ldp, int k,
+                                                T* __restrict__ c, double* __restrict__ hcol,
+                                                unsigned char* smem_raw);
+
 template <class T>
 __global__ void __launch_bounds__(256)
 fsub_panel_kernel(const T* __restrict__ u, const long long* __restrict__ pos, long long pos_offset,
@@ -155,6 +167,14 @@ fsub_panel_kernel(const T* __restrict__ u, const long long* __restrict__ pos, lo
   if (st->bd_iter != 0 && st->bd_iter < iter) return;
   if (side == 1 && st->bd_iter == iter) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  fsub_panel_body<T>(u, pos, pos_offset, P, ldp, k, c, hcol, smem_raw);
+}
+
+template <class T>
+__device__ __forceinline__ void fsub_panel_body(const T* __restrict__ u, const long long* __restrict__ pos,
+                                                long long pos_offset, const T* __restrict__ P, int ldp, int k,
+                                                T* __restrict__ c, double* __restrict__ hcol,
+                                                unsigned char* smem_raw) {
   T* v = reinterpret_cast<T*>(smem_raw);  // k values
   T* pan[2] = {v + k, v + k + 32 * k};    // two panels of <= 32 x k
   const int nbt = (k + 31) / 32;
@@ -251,6 +271,13 @@ template <> struct VecLoad<__nv_bfloat16, 8> {
 // plus argmax |u'| and sum (x - x_true)^2 partials; the last block to finish
 // reduces the partials (fixed order) into st->piv_* / relerr slot.
 template <class T, class B, int VEC, bool XF>
+__device__ __forceinline__ void elim_strips(long long n, long long idx_offset, const B* __restrict__ basis, long long ld,
+                                            int k, const T* cs, const T* u, int kx, const double* ys,
+                                            double* __restrict__ xout, const double* __restrict__ x0,
+                                            const double* __restrict__ xt, int write_u, T* uo, Cand& best,
+                                            double& sq);
+
+template <class T, class B, int VEC, bool XF>
 __global__ void __launch_bounds__(256)
 elim_pass_kernel(long long n, long long idx_offset, const B* __restrict__ basis, long long ld,
                  const int* __restrict__ kptr, int kfixed, const T* __restrict__ cvec, const T* u,
@@ -274,6 +301,50 @@ elim_pass_kernel(long long n, long long idx_offset, const B* __restrict__ basis,
 
   Cand best{-1.0, 0.0, 0x7fffffffffffffffLL};
   double sq = 0.0;
+  elim_strips<T, B, VEC, XF>(n, idx_offset, basis, ld, k, cs, u, kx, ys, xout, x0, xt, write_u, uo, best, sq);
+  best = block_argmax(best, scratch);
+  if (XF && kx > 0 && xt) sq = block_sum(sq, dscratch);
+  if (threadIdx.x == 0) {
+    cand_part[blockIdx.x] = best;
+    if (XF && kx > 0 && xt) xpart[blockIdx.x] = sq;
+    __threadfence();
+    const unsigned prev = atomicAdd(&st->counter[side], 1u);
+    am_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  Cand b2{-1.0, 0.0, 0x7fffffffffffffffLL};
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) {
+    Cand c;
+    c.mag = __ldcg(&cand_part[i].mag);
+    c.val = __ldcg(&cand_part[i].val);
+    c.idx = __ldcg(&cand_part[i].idx);
+    cand_merge(b2, c);
+  }
+  b2 = block_argmax(b2, scratch);
+  if (XF && kx > 0 && xt && relerr_out) {
+    // fixed-order parallel sum of the block partials (deterministic)
+    double s = 0.0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) s += __ldcg(&xpart[i]);
+    s = block_sum(s, dscratch);
+    if (threadIdx.x == 0) *relerr_out = s;  // squared norm; the host divides by |x_true|
+  }
+  if (threadIdx.x == 0) {
+    st->piv_val[side] = b2.val;
+    st->piv_idx[side] = b2.idx;
+    st->counter[side] = 0;
+  }
+}
+
+// the strips of one thread (grid-stride over the VEC-wide strips): in-order
+// elimination, fused iterate, running argmax candidate and error partial
+template <class T, class B, int VEC, bool XF>
+__device__ __forceinline__ void elim_strips(long long n, long long idx_offset, const B* __restrict__ basis, long long ld,
+                                            int k, const T* cs, const T* u, int kx, const double* ys,
+                                            double* __restrict__ xout, const double* __restrict__ x0,
+                                            const double* __restrict__ xt, int write_u, T* uo, Cand& best,
+                                            double& sq) {
   const long long nvec = (n + VEC - 1) / VEC;
   // one VEC-wide strip per thread (grid covers the vector exactly: no tail wave)
   for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < nvec;
@@ -321,39 +392,6 @@ elim_pass_kernel(long long n, long long idx_offset, const B* __restrict__ basis,
         }
       }
     }
-  }
-  best = block_argmax(best, scratch);
-  if (XF && kx > 0 && xt) sq = block_sum(sq, dscratch);
-  if (threadIdx.x == 0) {
-    cand_part[blockIdx.x] = best;
-    if (XF && kx > 0 && xt) xpart[blockIdx.x] = sq;
-    __threadfence();
-    const unsigned prev = atomicAdd(&st->counter[side], 1u);
-    am_last = (prev == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!am_last) return;
-  __threadfence();
-  Cand b2{-1.0, 0.0, 0x7fffffffffffffffLL};
-  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) {
-    Cand c;
-    c.mag = __ldcg(&cand_part[i].mag);
-    c.val = __ldcg(&cand_part[i].val);
-    c.idx = __ldcg(&cand_part[i].idx);
-    cand_merge(b2, c);
-  }
-  b2 = block_argmax(b2, scratch);
-  if (XF && kx > 0 && xt && relerr_out) {
-    // fixed-order parallel sum of the block partials (deterministic)
-    double s = 0.0;
-    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) s += __ldcg(&xpart[i]);
-    s = block_sum(s, dscratch);
-    if (threadIdx.x == 0) *relerr_out = s;  // squared norm; the host divides by |x_true|
-  }
-  if (threadIdx.x == 0) {
-    st->piv_val[side] = b2.val;
-    st->piv_idx[side] = b2.idx;
-    st->counter[side] = 0;
   }
 }
 
@@ -410,6 +448,145 @@ normalize_kernel(long long n, long long n_pad, const T* __restrict__ u, const T*
     // the next A^T apply's input, already in the blocked sinogram layout
     if (yb != nullptr && e < n) yb[blk.map(e)] = v;
   }
+}
+
+// --------------------------------------------------------------------------
+// One basis step as ONE cooperative kernel, for short vectors (configs 1-3,
+// where the step is a chain of latency-bound launches): forward substitution
+// (block 0) | grid barrier | elimination pass with the fused iterate and the
+// per-block argmax candidates (all blocks) | barrier | candidate merge, error
+// sum, pivot commit (block 0) | barrier | normalisation (all blocks).  Every
+// phase runs the device code of the separate kernels above on the same
+// operands in the same order, so pivots, H / W, P and the bases are
+// bit-identical to the launch-per-phase path (the relative-error sum alone is
+// grouped by this kernel's grid).  Not used with sampled pivoting (the sample
+// pick sits between the pass and the commit) or on shards.
+template <class T, class B>
+struct StepArgs {
+  // forward substitution
+  const T* u;            // operator output (read by fsub and the pass)
+  const T* P;            // pivot-row matrix (read), column-major ldp
+  T* Pw;                 // the same matrix (row k written by the commit)
+  int ldp, k;
+  T* c;                  // elimination coefficients (k)
+  double* hcol;          // H(:, k-1) or W(:, k): entries 0..k-1 by fsub, entry k by the commit
+  // elimination pass
+  long long n, ld;
+  const B* basis;
+  T* uo;                 // eliminated vector
+  int kx;
+  const double* yx;
+  const double* x0;
+  const double* xt;
+  double* xpart;
+  double* relerr_out;
+  Cand* cand;
+  // commit
+  long long dim;
+  long long* pos;
+  T* pivval;
+  // normalisation (do_norm = 0: the caller normalises with its own kernel)
+  int do_norm;
+  long long n_pad;
+  B* dst;
+  SinoBlk blk;
+  B* yb;
+  LoopState* st;
+  int side, iter;
+};
+
+template <class T, class B, bool XF>
+__global__ void __launch_bounds__(256, 2)
+basis_step_kernel(const StepArgs<T, B> a) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  LoopState* st = a.st;
+  // uniform over the grid (nothing below changes bd_iter before the last barrier but block 0's commit)
+  if (st->bd_iter != 0 && st->bd_iter < a.iter) return;
+  if (a.side == 1 && st->bd_iter == a.iter) return;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ Cand scratch[32];
+  __shared__ double dscratch[32];
+  __shared__ Cand winner;
+  const int k = a.k;
+  if (blockIdx.x == 0) fsub_panel_body<T>(a.u, a.pos, 0, a.P, a.ldp, k, a.c, a.hcol, smem_raw);
+  grid.sync();
+  T* cs = reinterpret_cast<T*>(smem_raw);
+  double* ys = reinterpret_cast<double*>(smem_raw + ((k * sizeof(T) + 15) / 16) * 16);
+  for (int i = threadIdx.x; i < k; i += blockDim.x) cs[i] = __ldcg(a.c + i);
+  for (int i = threadIdx.x; i < a.kx; i += blockDim.x) ys[i] = a.yx[i];
+  __syncthreads();
+  Cand best{-1.0, 0.0, 0x7fffffffffffffffLL};
+  double sq = 0.0;
+  elim_strips<T, B, 1, XF>(a.n, 0, a.basis, a.ld, k, cs, a.u, a.kx, ys, nullptr, a.x0, a.xt, 1, a.uo, best, sq);
+  best = block_argmax(best, scratch);
+  const bool err = XF && a.kx > 0 && a.xt;
+  if (err) sq = block_sum(sq, dscratch);
+  if (threadIdx.x == 0) {
+    a.cand[blockIdx.x] = best;
+    if (err) a.xpart[blockIdx.x] = sq;
+  }
+  grid.sync();
+  if (blockIdx.x == 0) {
+    Cand b2{-1.0, 0.0, 0x7fffffffffffffffLL};
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) {
+      Cand c;
+      c.mag = __ldcg(&a.cand[i].mag);
+      c.val = __ldcg(&a.cand[i].val);
+      c.idx = __ldcg(&a.cand[i].idx);
+      cand_merge(b2, c);
+    }
+    b2 = block_argmax(b2, scratch);
+    if (err && a.relerr_out) {
+      double s = 0.0;
+      for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) s += __ldcg(&a.xpart[i]);
+      s = block_sum(s, dscratch);
+      if (threadIdx.x == 0) *a.relerr_out = s;
+    }
+    if (threadIdx.x == 0) {
+      st->piv_val[a.side] = b2.val;
+      st->piv_idx[a.side] = b2.idx;
+      winner = b2;
+    }
+    __syncthreads();
+    // the commit (pivot_commit_kernel) on the winner
+    const double val = (k < a.dim) ? winner.val : 0.0;
+    const long long idx = winner.idx;
+    if (val == 0.0) {
+      if (threadIdx.x == 0) {
+        a.hcol[k] = 0.0;
+        st->bd_iter = a.iter;
+        st->bd_side = a.side;
+      }
+    } else {
+      if (threadIdx.x == 0) {
+        a.hcol[k] = val;
+        a.pos[k] = idx;
+        *a.pivval = (T)val;
+      }
+      for (int i = threadIdx.x; i <= k; i += blockDim.x) {
+        T pv;
+        if (i == k) pv = T(1);
+        else pv = (idx >= 0 && idx < a.n) ? cvt<T>(a.basis[(long long)i * a.ld + idx]) : T(0);
+        a.Pw[(long long)i * a.ldp + k] = pv;
+      }
+    }
+  }
+  grid.sync();
+  if (!a.do_norm) return;
+  if (__ldcg(&st->bd_iter) != 0 && __ldcg(&st->bd_iter) <= a.iter) return;  // block 0's commit may have set it
+  const T p = __ldcg(a.pivval);
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < a.n_pad;
+       e += (long long)gridDim.x * blockDim.x) {
+    const B v = (e < a.n) ? cvt<B>(Rn<T>::div(__ldcg(a.uo + e), p)) : cvt<B>(T(0));
+    a.dst[e] = v;
+    if (a.yb != nullptr && e < a.n) a.yb[a.blk.map(e)] = v;
+  }
+}
+
+inline size_t basis_step_smem(int k, int kx, size_t tsize) {
+  const size_t elim = ((k * tsize + 15) / 16) * 16 + (size_t)kx * sizeof(double) + 16;
+  return std::max(fsub_panel_smem(k, tsize), elim);
 }
 
 // The same normalisation for a grid x grid image vector (tomography L side),

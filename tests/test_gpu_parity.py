@@ -610,6 +610,55 @@ def test_deterministic_replay(hs):
     assert r1.trace.column("proj_obj") == r2.trace.column("proj_obj")
 
 
+@pytest.mark.parametrize("case", ["tomo_f32_lam", "tomo_f64", "psf_bf16", "dense_breakdown"])
+def test_fused_basis_step_matches_separate_kernels(hs, monkeypatch, case):
+    """The cooperative basis-step kernel (forward substitution | pass | commit |
+    normalisation in one launch, short vectors) against the launch-per-phase
+    path (HS_NO_STEP_FUSE=1): pivots, H, W, the bases, y-dependent outputs x /
+    sres / proj_obj bit for bit; rel_err (a sum grouped by the grid) to 1e-12."""
+    from paper_2502_02721_b200.problems import add_noise, gaussian_psf, random_ellipses, rectangles_and_discs
+
+    if case.startswith("tomo"):
+        dt = np.float32 if case == "tomo_f32_lam" else np.float64
+        op = hs.TomographyOperator(40, 30, 57, dtype=dt)
+        x = random_ellipses(40, 8, 1).ravel()
+        b, _ = add_noise(op.matvec(x), 0.01, 2)
+        cfg = hs.SolverConfig(maxiter=25, lam=1e-3 if case == "tomo_f32_lam" else 0.0,
+                              dtype="float32" if dt == np.float32 else "float64", sketch_kind="sparse_sign")
+        solve = hs.slslu
+    elif case == "psf_bf16":
+        op = hs.PsfOperator(48, gaussian_psf(1.5, radius=5), dtype=np.float32)
+        x = rectangles_and_discs(48, 12, 0).ravel()
+        b, _ = add_noise(op.matvec(x), 0.01, 1)
+        cfg = hs.SolverConfig(maxiter=30, sketch_rows=120, dtype="float32", basis_dtype="bfloat16",
+                              sketch_kind="gaussian")
+        solve = hs.scmrh
+    else:  # exact breakdown: a rank-6 dense operator runs out of pivots
+        rng = np.random.default_rng(4)
+        M = rng.standard_normal((40, 6)) @ rng.standard_normal((6, 40))
+        op = hs.DenseOperator(M)
+        x = np.ones(40)
+        b = M @ x
+        cfg = hs.SolverConfig(maxiter=12, sketch_rows=60)
+        solve = hs.scmrh
+    got = solve(op, b, cfg, x_true=x)
+    monkeypatch.setenv("HS_NO_STEP_FUSE", "1")
+    ref = solve(op, b, cfg, x_true=x)
+    assert got.termination == ref.termination and len(got.trace.records) == len(ref.trace.records)
+    fa, fb = got.factorization, ref.factorization
+    np.testing.assert_array_equal(fa.t, fb.t)
+    np.testing.assert_array_equal(fa.H_matrix(), fb.H_matrix())
+    np.testing.assert_array_equal(fa.L_matrix(), fb.L_matrix())
+    if solve is hs.slslu:
+        np.testing.assert_array_equal(fa.g, fb.g)
+        np.testing.assert_array_equal(fa.W_matrix(), fb.W_matrix())
+        np.testing.assert_array_equal(fa.D_matrix(), fb.D_matrix())
+    np.testing.assert_array_equal(got.x, ref.x)
+    for name in ("sres_norm", "proj_obj"):
+        np.testing.assert_array_equal(got.trace.column(name), ref.trace.column(name))
+    np.testing.assert_allclose(got.trace.column("rel_err"), ref.trace.column("rel_err"), rtol=1e-12)
+
+
 def test_sketch_basis_matches_column_sketching(hs):
     rng = np.random.default_rng(22)
     M = rng.standard_normal((14, 14)) + 4 * np.eye(14)
