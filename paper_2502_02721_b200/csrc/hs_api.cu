@@ -999,11 +999,11 @@ struct hs_op {
       constexpr int TX = 32, TY = 8;
       dim3 grid((W + TX - 1) / TX, (out_rows + TY - 1) / TY);
       const size_t smem = ((size_t)(TX + 2 * (kw / 2)) * (TY + 2 * (kh / 2)) + (size_t)kh * kw) * sizeof(T);
-      if (smem > 48 * 1024)
-        CK(cudaFuncSetAttribute(psf_stencil_kernel<V, Tin, T, TX, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
-      psf_stencil_kernel<V, Tin, T, TX, TY><<<grid, TX * TY, smem, s>>>(rows, W, kh, kw, K.as<V>(), xi, yo,
-                                                                         transpose ? 1 : 0, out_row0, out_rows);
+      // 15-wide rows unrolled (config 2: 19 -> see DESIGN.md); other widths generic
+      auto kern = kw == 15 && !env_flag("HS_PSF_GENERIC") ? psf_stencil_kernel<V, Tin, T, TX, TY, 15>
+                                                          : psf_stencil_kernel<V, Tin, T, TX, TY, 0>;
+      CK(ensure_smem((const void*)kern, smem));
+      kern<<<grid, TX * TY, smem, s>>>(rows, W, kh, kw, K.as<V>(), xi, yo, transpose ? 1 : 0, out_row0, out_rows);
       CKL();
     }
   }

@@ -172,10 +172,14 @@ inline size_t dense_tile_smem(size_t tsize, int rb, int ct) { return ((size_t)rb
 // Output rows [out_row0, out_row0 + out_rows) of the H-row image x are written
 // to y[(r - out_row0) * W + c] (a row-sharded rank passes its rows plus the
 // neighbours' halo rows as x and computes only its own rows).
-template <class V, class Tin, class T, int TILE_X, int TILE_Y>
+// KWC > 0: the PSF width as a compile-time constant (the tap loop unrolls and
+// its shared-memory reads batch: config 2's 15 x 15 stencil on a 256^2 image);
+// KWC = 0: any width.  Same taps in the same order either way.
+template <class V, class Tin, class T, int TILE_X, int TILE_Y, int KWC = 0>
 __global__ void __launch_bounds__(TILE_X * TILE_Y)
-psf_stencil_kernel(int H, int W, int kh, int kw, const V* __restrict__ K,
+psf_stencil_kernel(int H, int W, int kh, int kw_rt, const V* __restrict__ K,
                    const Tin* __restrict__ x, T* __restrict__ y, int transpose, int out_row0, int out_rows) {
+  const int kw = KWC > 0 ? KWC : kw_rt;
   extern __shared__ unsigned char smem_raw[];
   const int ry = kh / 2, rx = kw / 2;
   const int SW = TILE_X + 2 * rx, SH = TILE_Y + 2 * ry;
@@ -200,14 +204,24 @@ psf_stencil_kernel(int H, int W, int kh, int kw, const V* __restrict__ K,
     for (int a = 0; a < kh; ++a) {
       const T* trow = tile + (ty + 2 * ry - a) * SW + tx + 2 * rx;
       const T* krow = ks + a * kw;
-      for (int b = 0; b < kw; ++b) acc = Rn<T>::add(acc, Rn<T>::mul(krow[b], trow[-b]));
+      if (KWC > 0) {
+#pragma unroll
+        for (int b = 0; b < KWC; ++b) acc = Rn<T>::add(acc, Rn<T>::mul(krow[b], trow[-b]));
+      } else {
+        for (int b = 0; b < kw; ++b) acc = Rn<T>::add(acc, Rn<T>::mul(krow[b], trow[-b]));
+      }
     }
   } else {
     // out[r,c] = sum_a sum_b K[a,b] x[r - ry + a, c - rx + b]
     for (int a = 0; a < kh; ++a) {
       const T* trow = tile + (ty + a) * SW + tx;
       const T* krow = ks + a * kw;
-      for (int b = 0; b < kw; ++b) acc = Rn<T>::add(acc, Rn<T>::mul(krow[b], trow[b]));
+      if (KWC > 0) {
+#pragma unroll
+        for (int b = 0; b < KWC; ++b) acc = Rn<T>::add(acc, Rn<T>::mul(krow[b], trow[b]));
+      } else {
+        for (int b = 0; b < kw; ++b) acc = Rn<T>::add(acc, Rn<T>::mul(krow[b], trow[b]));
+      }
     }
   }
   y[(long long)(r - out_row0) * W + c] = acc;
