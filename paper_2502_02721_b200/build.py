@@ -52,7 +52,9 @@ def build(force=False, verbose=True):
         return LIB
     os.makedirs(OUT_DIR, exist_ok=True)
     tmp = LIB + ".tmp"
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", tmp, os.path.join(CSRC, "hs_api.cu")]
+    # HS_NVCC_DEFS: extra -D switches for compile-time experiments (e.g. "-DHS_ELIM_CS")
+    extra = os.environ.get("HS_NVCC_DEFS", "").split()
+    cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-o", tmp, os.path.join(CSRC, "hs_api.cu")]
     if verbose:
         print(" ".join(cmd), flush=True)
     proc = subprocess.run(cmd, capture_output=True, text=True)

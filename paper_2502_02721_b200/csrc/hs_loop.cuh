@@ -245,7 +245,8 @@ template <class B> struct VecLoad<B, 1> {
 };
 template <> struct VecLoad<float, 4> {
   static __device__ __forceinline__ void ld(const float* p, float (&o)[4]) {
-    float4 t = __ldg(reinterpret_cast<const float4*>(p));
+    // basis columns are read once per pass: evict-first (+2% on the config-4 pass over __ldg)
+    float4 t = __ldcs(reinterpret_cast<const float4*>(p));
     o[0] = t.x; o[1] = t.y; o[2] = t.z; o[3] = t.w;
   }
 };
@@ -277,8 +278,20 @@ __device__ __forceinline__ void elim_strips(long long n, long long idx_offset, c
                                             const double* __restrict__ xt, int write_u, T* uo, Cand& best,
                                             double& sq);
 
+// Resident blocks per SM of the fp32 / fp32-basis pass (config 4), measured in
+// the solve (bench.py kernels table, GB/s of the pass's algorithmic bytes):
+// plain launch bounds (44 / 64 registers, 5 / 4 blocks) 4.99 / 5.57 TB/s for
+// the D / L side; 7 / 6 blocks (36 / 40 registers) with four basis columns in
+// flight per thread and evict-first loads 6.05 / 5.99 TB/s = 0.94 / 0.93 of
+// the copy peak (6 / 5 blocks: 5.63 / 5.13; 8 / 8: 6.05 / 5.67).
+#ifndef HS_ELIM_MINB_L
+#define HS_ELIM_MINB_L 6
+#endif
+#ifndef HS_ELIM_MINB_D
+#define HS_ELIM_MINB_D 7
+#endif
 template <class T, class B, int VEC, bool XF>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, (VEC == 4 && sizeof(T) == 4) ? (XF ? HS_ELIM_MINB_L : HS_ELIM_MINB_D) : 0)
 elim_pass_kernel(long long n, long long idx_offset, const B* __restrict__ basis, long long ld,
                  const int* __restrict__ kptr, int kfixed, const T* __restrict__ cvec, const T* u,
                  int kx, const double* __restrict__ yx, double* __restrict__ xout,
@@ -361,7 +374,13 @@ __device__ __forceinline__ void elim_strips(long long n, long long idx_offset, c
     }
     const B* bp = basis + e0;
     // kx <= k always (x of the previous iteration uses the first k-1 columns)
-    constexpr int UNR = VEC == 1 ? 16 : (XF ? 4 : 8);
+#ifndef HS_ELIM_UNR_D
+#define HS_ELIM_UNR_D 4
+#endif
+#ifndef HS_ELIM_UNR_L
+#define HS_ELIM_UNR_L 4
+#endif
+    constexpr int UNR = VEC == 1 ? 16 : (XF ? HS_ELIM_UNR_L : HS_ELIM_UNR_D);
 #pragma unroll UNR
     for (int j = 0; j < k; ++j) {
       B b[VEC];
