@@ -843,7 +843,10 @@ struct hs_op {
         if (img_grid > 0 && (img_grid & (img_grid - 1)) == 0) gshift = __builtin_ctz((unsigned)img_grid);
         const bool p2 = gshift >= 0 || !tflag;
         constexpr bool F32 = sizeof(T) == 4 && sizeof(V) == 4;
-        constexpr int MINB = F32 ? 6 : 3;
+#ifndef HS_C2_MINB
+#define HS_C2_MINB 6
+#endif
+        constexpr int MINB = F32 ? HS_C2_MINB : 3;
         // (8 blocks per SM, 32 registers with 40 B of spills: 3.17 against 2.78 ms)
         auto kern = p2 ? sell_spmv_c2_kernel<V, Tin, T, true, MINB> : sell_spmv_c2_kernel<V, Tin, T, false, MINB>;
         kern<<<grid, 256, 0, s>>>(M.rows, M.nslices, M.sptr.as<long long>(), M.rlen.as<int>(), M.rbase.as<int>(),

@@ -989,7 +989,10 @@ sell_spmv_imp_kernel(long long rows, long long nslices, const long long* __restr
 }
 
 template <class V, class Tin, class T, bool POW2, int DEPTH = 0>
-__global__ void __launch_bounds__(256, (DEPTH == 0 || DEPTH == 3) ? ((sizeof(T) == 4 && sizeof(V) == 4) ? 6 : 3)
+#ifndef HS_D16_MINB
+#define HS_D16_MINB 6
+#endif
+__global__ void __launch_bounds__(256, (DEPTH == 0 || DEPTH == 3) ? ((sizeof(T) == 4 && sizeof(V) == 4) ? HS_D16_MINB : 3)
                                        : DEPTH == 1 ? ((sizeof(T) == 4 && sizeof(V) == 4) ? 4 : 2)
                                        : DEPTH == 2 ? 2 : 1)
 sell_spmv_d16_kernel(long long rows, long long nslices, const long long* __restrict__ sptr,
