@@ -1713,7 +1713,7 @@ struct Solver {
       CK(cudaMemcpyAsync(P, &one, sizeof(T), cudaMemcpyHostToDevice, s));
       CK(cudaStreamSynchronize(s));
     };
-    const int NORM_G = SMS * 8;
+    const int NORM_G = SMS * env_int("HS_NORM_BLOCKS", 8);
 
     int tmat0 = 0, sk0 = 0;
     double beta, alpha = 0.0;

@@ -460,12 +460,24 @@ normalize_kernel(long long n, long long n_pad, const T* __restrict__ u, const T*
                  SinoBlk blk = SinoBlk{0, 0, 0, 0}, B* __restrict__ yb = nullptr) {
   if (st->bd_iter != 0 && st->bd_iter <= iter) return;
   const T p = *pivval;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n_pad;
-       e += (long long)gridDim.x * blockDim.x) {
-    const B v = (e < n) ? cvt<B>(Rn<T>::div(u[e], p)) : cvt<B>(T(0));
-    dst[e] = v;
-    // the next A^T apply's input, already in the blocked sinogram layout
-    if (yb != nullptr && e < n) yb[blk.map(e)] = v;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  // four grid-strided elements per step: their loads are in flight together
+  for (long long e0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; e0 < n_pad; e0 += 4 * stride) {
+    T uu[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const long long e = e0 + i * stride;
+      uu[i] = e < n ? u[e] : T(0);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const long long e = e0 + i * stride;
+      if (e >= n_pad) break;
+      const B v = (e < n) ? cvt<B>(Rn<T>::div(uu[i], p)) : cvt<B>(T(0));
+      dst[e] = v;
+      // the next A^T apply's input, already in the blocked sinogram layout
+      if (yb != nullptr && e < n) yb[blk.map32((int)e)] = v;
+    }
   }
 }
 
@@ -599,7 +611,7 @@ basis_step_kernel(const StepArgs<T, B> a) {
        e += (long long)gridDim.x * blockDim.x) {
     const B v = (e < a.n) ? cvt<B>(Rn<T>::div(__ldcg(a.uo + e), p)) : cvt<B>(T(0));
     a.dst[e] = v;
-    if (a.yb != nullptr && e < a.n) a.yb[a.blk.map(e)] = v;
+    if (a.yb != nullptr && e < a.n) a.yb[a.blk.map32((int)e)] = v;
   }
 }
 
