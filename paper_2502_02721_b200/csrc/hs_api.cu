@@ -760,7 +760,10 @@ struct hs_op {
     T* yo = reinterpret_cast<T*>(y);
     if (kind == OP_CSR && (transpose ? Ats.nslices : As.nslices) > 0) {
       const Sell& M = transpose ? Ats : As;
-      const int grid = grid_for(M.nslices, 8, ctx->num_sms * 16);
+      // blocks per SM of the dynamically scheduled SpMV kernels: the resident count (6 at fp32) rather
+      // than a longer grid whose late blocks start only to find the slice counter exhausted
+      // (config 4 in the solve: 130.1 -> 130.3 it/s; 12 and 32 per SM: no better)
+      const int grid = grid_for(M.nslices, 8, ctx->num_sms * env_int("HS_SPMV_GRID", 6));
       // algorithmic bytes of the stored encoding: values + column indices (4 B, or 2 B deltas)
       // + row lengths (+ row bases) + slice pointers + x once + y
       const bool impl = !transpose && imp_slices > 0 && M.d16 && !M.d16v && !M.c8;
