@@ -646,11 +646,15 @@ static void csr_to_sell(hs_ctx* ctx, const Csr& A, Sell& S, int tile_grid = 0) {
   S.nnz = A.nnz;
   if (tile_grid > 0) {
     const long long rows_img = (A.rows + tile_grid - 1) / tile_grid;  // image rows in this block
-    const long long tiles = (long long)((tile_grid + 7) / 8) * ((rows_img + 3) / 4);
+    // tile shape tw x (32 / tw): 8 x 4 by default (HS_AT_TILE_W = 4 or 16 for A/B runs)
+    int tw = env_int("HS_AT_TILE_W", 8);
+    if (tw != 4 && tw != 16) tw = 8;
+    const int th = 32 / tw;
+    const long long tiles = (long long)((tile_grid + tw - 1) / tw) * ((rows_img + th - 1) / th);
     S.nslices = tiles;
     S.rperm.alloc(S.nslots() * sizeof(int), false);
     tile_perm_block_kernel<<<grid_for(S.nslots(), 256, 1 << 30), 256, 0, s>>>(
-        tile_grid, (int)((A.rows + tile_grid - 1) / tile_grid), S.nslots(), S.rperm.as<int>());
+        tile_grid, (int)((A.rows + tile_grid - 1) / tile_grid), S.nslots(), S.rperm.as<int>(), tw);
     CKL();
   } else {
     S.nslices = (A.rows + 31) / 32;

@@ -112,14 +112,16 @@ __global__ void iota_kernel(long long* __restrict__ a, int n) {
 }
 
 // slot -> local pixel for 8x4 tiles over an image block of `rows_img` rows
-__global__ void tile_perm_block_kernel(int grid, int rows_img, long long nslots, int* __restrict__ rperm) {
+// tw: tile width in pixels (4, 8 or 16; the tile is tw x 32 / tw)
+__global__ void tile_perm_block_kernel(int grid, int rows_img, long long nslots, int* __restrict__ rperm, int tw = 8) {
   const long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (slot >= nslots) return;
-  const int tiles_x = (grid + 7) / 8;
+  const int th = 32 / tw;
+  const int tiles_x = (grid + tw - 1) / tw;
   const long long tile = slot >> 5;
   const int lane = (int)(slot & 31);
   const long long ty = tile / tiles_x, tx = tile % tiles_x;
-  const long long r = ty * 4 + (lane >> 3), c = tx * 8 + (lane & 7);
+  const long long r = ty * th + lane / tw, c = tx * tw + lane % tw;
   rperm[slot] = (r < rows_img && c < grid) ? (int)(r * grid + c) : -1;
 }
 
